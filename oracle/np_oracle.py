@@ -1,0 +1,159 @@
+"""numpy fp64 oracle for large tori -- TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Same definitions as holo_oracle.c (O3..O12), with two library
+primitives standing in for naive sums so that L = 2048 / 4096 frames finish in
+seconds: ``numpy.fft`` for the DFT (O2) and a dense matrix product for the O5
+evaluation sum.  Nothing here is blocked, fused or reordered beyond that.
+
+    O5:  Xc[f] = sum_n x[n] e^{-2 pi i fbar u(n)/L} = e^{i pi fbar} FFT(x)[f]   (u(n) = n - L/2)
+         y[n]  = (1/L) sum_f E[n, f] kappa[f] r_s[f] Xc[f],  E[n, f] = e^{+2 pi i mt fbar u(n)/L}
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def fbar(L):
+    f = np.arange(L)
+    return np.where(f < L // 2, f, f - L)
+
+
+def transfer(L, wavelength, p0, z):
+    """O3: h_z[f] = exp(-i pi lambda z (fbar/(L p0))^2)."""
+    fr = fbar(L) / (L * p0)
+    return np.exp(-1j * np.pi * wavelength * z * fr * fr)
+
+
+def ramp(L, s):
+    """O4: r_s[f] = exp(-2 pi i fbar s / L)."""
+    return np.exp(-2j * np.pi * fbar(L) * s / L)
+
+
+def kappa(L, mt):
+    v = mt * fbar(L)
+    return ((v >= -(L // 2)) & (v < L // 2)).astype(np.float64)
+
+
+def prop(x, wavelength, p0, z):
+    L = x.shape[-1]
+    h = transfer(L, wavelength, p0, z)
+    return np.fft.ifft2(np.fft.fft2(x) * h[:, None] * h[None, :])
+
+
+def shift(x, sx, sy):
+    L = x.shape[-1]
+    return np.fft.ifft2(np.fft.fft2(x) * ramp(L, sy)[:, None] * ramp(L, sx)[None, :])
+
+
+class MagOp:
+    """O5 for one (L, mt): E[n, f] = exp(+2 pi i mt fbar u(n) / L), phase reduced mod L."""
+
+    def __init__(self, L, mt):
+        self.L, self.mt = L, float(mt)
+        u = np.arange(L) - L // 2
+        fb = fbar(L)
+        p = self.mt * (u[:, None] * fb[None, :]).astype(np.float64)
+        p -= L * np.floor(p / L)
+        self.E = np.exp(2j * np.pi * p / L)
+        self.kap = kappa(L, mt)
+        self.centre = np.exp(1j * np.pi * fb)  # e^{i pi fbar} = (-1)^fbar
+
+    def _axis_fwd(self, x, s, axis):
+        X = np.fft.fft(x, axis=axis)
+        c = self.centre * self.kap * ramp(self.L, s)
+        if axis == 1:
+            return (X * c[None, :]) @ self.E.T / self.L
+        return self.E @ (X * c[:, None]) / self.L
+
+    def _axis_adj(self, y, s, axis):
+        c = np.conj(self.centre) * self.kap * np.conj(ramp(self.L, s))
+        if axis == 1:
+            Zf = y @ np.conj(self.E)
+            return np.fft.ifft(Zf * c[None, :], axis=1)
+        Zf = np.conj(self.E).T @ y
+        return np.fft.ifft(Zf * c[:, None], axis=0)
+
+    def fwd(self, x, sx, sy):
+        """M_{1/mt} S_(sx,sy) x: along x with sx, then along y with sy."""
+        return self._axis_fwd(self._axis_fwd(x, sx, 1), sy, 0)
+
+    def adj(self, y, sx, sy):
+        return self._axis_adj(self._axis_adj(y, sy, 0), sx, 1)
+
+
+def crop(x, N):
+    L = x.shape[-1]
+    o = (L - N) // 2
+    return x[..., o:o + N, o:o + N]
+
+
+def zpad(x, L):
+    N = x.shape[-1]
+    o = (L - N) // 2
+    out = np.zeros(x.shape[:-2] + (L, L), np.complex128)
+    out[..., o:o + N, o:o + N] = x
+    return out
+
+
+class Problem:
+    """Frame-level forward / residual / gradient contributions (O6..O12).
+
+    ``geom`` carries wavelength, p0, mt[], zdet[], omega[] (oracle.Geometry)."""
+
+    def __init__(self, geom, L, N):
+        self.g, self.L, self.N = geom, L, N
+        self._mag = {}
+
+    def mag(self, j):
+        if j not in self._mag:
+            self._mag[j] = MagOp(self.L, self.g.mt[j])
+        return self._mag[j]
+
+    def qj(self, q, j):
+        return prop(q, self.g.wavelength, self.g.p0, self.g.omega[j])
+
+    def frame_fwd(self, psi_k, qj, j, s):
+        a = self.mag(j).fwd(psi_k, s[0], s[1])
+        return crop(prop(qj * a, self.g.wavelength, self.g.p0, self.g.zdet[j]), self.N), a
+
+    def frame_grad(self, psi_k, qj, j, s, sqrt_d):
+        """One frame (k, j): returns F_kj, 2 L_kj^* rho, and conj(a) v (the G_j term, no 2, no P_{-omega})."""
+        w, a = self.frame_fwd(psi_k, qj, j, s)
+        m = np.abs(w)
+        F = float(np.sum((m - sqrt_d) ** 2))
+        with np.errstate(invalid="ignore", divide="ignore"):
+            rho = np.where(m > 0, w - sqrt_d * w / np.where(m > 0, m, 1), 0)
+        v = prop(zpad(rho, self.L), self.g.wavelength, self.g.p0, -self.g.zdet[j])
+        gpsi = 2.0 * self.mag(j).adj(np.conj(qj) * v, s[0], s[1])
+        return F, gpsi, np.conj(a) * v
+
+    def grad(self, psi, q, shifts, sqrt_d, frames=None):
+        """F, grad_psi, grad_q over all frames (or a subset: list of (k, j))."""
+        K, nz = psi.shape[0], self.g.nz
+        frames = frames if frames is not None else [(k, j) for j in range(nz) for k in range(K)]
+        F = 0.0
+        gpsi = np.zeros_like(psi, dtype=np.complex128)
+        G = {}
+        qjs = {}
+        for (k, j) in frames:
+            if j not in qjs:
+                qjs[j] = self.qj(q, j)
+            Fk, gk, Gk = self.frame_grad(psi[k], qjs[j], j, shifts[k, j], sqrt_d[k, j])
+            F += Fk
+            gpsi[k] += gk
+            G[j] = G.get(j, 0) + Gk
+        gq = np.zeros((self.L, self.L), np.complex128)
+        for j in sorted(G):
+            gq += 2.0 * prop(G[j], self.g.wavelength, self.g.p0, -self.g.omega[j])
+        return F, gpsi, gq
+
+    def fwd(self, psi, q, shifts, frames=None):
+        K, nz = psi.shape[0], self.g.nz
+        frames = frames if frames is not None else [(k, j) for k in range(K) for j in range(nz)]
+        out = {}
+        qjs = {}
+        for (k, j) in frames:
+            if j not in qjs:
+                qjs[j] = self.qj(q, j)
+            out[(k, j)] = self.frame_fwd(psi[k], qjs[j], j, shifts[k, j])[0]
+        return out
