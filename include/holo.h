@@ -1,0 +1,180 @@
+/*
+ * holo.h -- C ABI of the B200 (sm_100a) hot path of arXiv 2407.20304,
+ * "X-ray nano-holotomography reconstruction with simultaneous probe retrieval".
+ *
+ * One iteration of the batched per-projection holography operator of Eq. (8)
+ * with the amplitude functional F1 of Eq. (10), its Wirtinger
+ * gradients Eqs. (11)-(12) and the pointwise half of the Dai-Yuan
+ * conjugate-gradient step Eqs. (13)-(14).  P:n = PAPER.md line n.
+ *
+ * Conventions (readings C1-C21):
+ *  - complex = float2 {re, im} (complex64); every array is row-major [y][x]
+ *    (x is the fast index); per-frame arrays are ordered [k][j][y][x], k = angle,
+ *    j = sample plane ("distance"), one (k, j) pair = one "frame".
+ *  - The object psi_k and probe q live on the npad x npad torus (2x padding, C3);
+ *    detector-plane fields and data live on the central n x n window,
+ *    offset o = (npad - n)/2 (crop C / zero-pad Z, O7).
+ *  - Pointers are DEVICE pointers unless marked [host].  The caller owns every
+ *    array buffer; the plan owns its tables and workspace.  No entry point
+ *    allocates per call.  Outputs must not alias inputs unless stated.
+ *  - Every call enqueues on the plan's stream and returns without synchronising;
+ *    scalar outputs stay on the device.
+ *  - Errors: all arguments are validated on the host before any launch and a
+ *    failure returns HOLO_EINVAL (bad pointer/size/geometry) or
+ *    HOLO_EUNSUPPORTED (valid but not implemented size).  A CUDA failure returns
+ *    HOLO_ECUDA and puts the plan in a sticky error state: later calls return
+ *    HOLO_ESTATE until holo_plan_destroy.  holo_last_error() gives the text.
+ *    No C++ exception crosses the ABI.
+ *  - A plan is single-threaded and bound to one (device, stream).
+ */
+#ifndef HOLO_H
+#define HOLO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct holo_plan holo_plan; /* opaque */
+
+typedef enum {
+  HOLO_OK = 0,
+  HOLO_EINVAL = -1,
+  HOLO_ENOMEM = -2,
+  HOLO_ECUDA = -3,
+  HOLO_EUNSUPPORTED = -4,
+  HOLO_ESTATE = -5
+} holo_status;
+
+#define HOLO_MAX_NZ 8
+
+/* Acquisition geometry (Table 1; Eq. (6); Eq. (8)). */
+typedef struct {
+  int32_t n;           /* detector / data side N: even, >= 8, n <= npad, (npad - n) even   */
+  int32_t npad;        /* torus side N_p: power of two, 128 <= npad <= 4096
+                          (6144 = 3*2^11 for reference-arm-only plans, n_angles == 0)          */
+  int32_t nz;          /* number of sample planes ("distances"), 1..HOLO_MAX_NZ               */
+  int32_t n_angles;    /* K: angles resident on this device (0: reference-arm-only plan)      */
+  int32_t angle_batch; /* reserved (sizes future batched workspace); pass 1                   */
+  double wavelength;   /* lambda [m] > 0                                                       */
+  double focus_to_detector; /* Z [m]                                                          */
+  double z1[HOLO_MAX_NZ];   /* focus-to-sample [m], 0 < z1[0] < ... < z1[nz-1] < Z            */
+  double detector_pixel;    /* [m] > 0; object-plane pixel p0 = detector_pixel * z1[0] / Z   */
+} holo_geometry;
+
+/* Create a plan on `device` that enqueues on `stream` (a cudaStream_t; NULL = legacy
+ * default stream).  Derives (O1): m0 = Z/z1_0, mt_j = z1_j/z1_0, zeta_j = z1_j(Z-z1_j)/Z,
+ * omega_j = (z1_j - z1_0)/mt_j, zdet_j = zeta_j/mt_j^2, p0 = det_px/m0 (Eq. (8)),
+ * builds the fp64-derived fp32 tables (Fresnel transfers, chirp-z chirps and kernel
+ * spectra, FFT twiddles) and allocates the workspace.  Errors: HOLO_EINVAL for a bad
+ * geometry, HOLO_EUNSUPPORTED for an npad outside the supported set, HOLO_ENOMEM. */
+holo_status holo_plan_create(holo_plan **out, const holo_geometry *g /*[host]*/, int device, void *stream);
+void holo_plan_destroy(holo_plan *p); /* NULL allowed */
+size_t holo_plan_workspace_bytes(const holo_plan *p);
+const char *holo_last_error(const holo_plan *p); /* message of the last non-OK status */
+
+/* Derived geometry (O1), all [host] arrays of length nz; any pointer may be NULL. */
+holo_status holo_plan_derived(const holo_plan *p, double *m0, double *mt, double *zdet, double *omega,
+                              double *zeta, double *p0);
+
+/* Sample shifts s^s_kj (Eq. (10), "S_{s^s_kj}"; reading C4): [host] float64
+ * [n_angles][nz][2] = (sx, sy) in object-plane (psi-grid) pixels, applied before the
+ * magnification, periodic on the torus; |s| < npad/2 and finite, else HOLO_EINVAL.
+ * Copied into the plan (the host buffer may be reused on return).  Default: all zero. */
+holo_status holo_set_shifts(holo_plan *p, const double *s /*[host]*/);
+
+/* Reference-frame shifts s^r_r (Eq. (10) reference term P:115; reading C16):
+ * [host] float64 [n_ref][2] = (sx, sy).  Sets R = n_ref for holo_grad_ref. */
+holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s /*[host]*/);
+
+/* Forward (O7, Eq. (8) without the detector-frame rescale, reading C8):
+ *   w[k][j] = C( P_{zdet_j}( q_j . M_{1/mt_j} S_{s_kj} psi_k ) ),  q_j = P_{omega_j} q.
+ * psi [K][npad][npad], q [npad][npad] -> w [K][nz][n][n].                                */
+holo_status holo_fwd(holo_plan *p, const void *psi, const void *q, void *w);
+
+/* Adjoints of the two linearisations at (psi, q) for a detector-plane field y:
+ *   adj_psi[k] = sum_j L_kj^* y_kj,   L_kj^* = S_{-s} M^*_{1/mt} (conj(q_j) . P_{-zdet_j} Z .)
+ *   adj_q      = sum_{k,j} Q_kj^* y_kj = sum_j P_{-omega_j} sum_k conj(M S psi_k) . P_{-zdet_j} Z y_kj
+ * (local partial over this plan's angles; no factor 2).  Either output may be NULL.     */
+holo_status holo_adj(holo_plan *p, const void *y /*[K][nz][n][n]*/, const void *psi, const void *q,
+                     void *adj_psi /*[K][npad][npad] | NULL*/, void *adj_q /*[npad][npad] | NULL*/);
+
+#define HOLO_ACCUMULATE_Q 1u  /* add into grad_q_part instead of overwriting          */
+#define HOLO_OBJECTIVE_ONLY 2u /* F only: no adjoint work, grad outputs ignored       */
+
+/* Fused sweep at (psi, q) over this plan's angles (O8-O12; Eqs. (10)-(12)).
+ * Writes fp64 DEVICE scalars sc[3]:
+ *   sc[0] = F_local = sum_{k,j} sum_pix (|w_kj| - sqrt_d_kj)^2                 (Eq. (10))
+ *   sc[1] = ||grad_psi||^2 over local angles
+ *   sc[2] = Re<grad_psi, eta_psi_prev> over local angles (0 if eta_psi_prev NULL) (Eq. (14))
+ * grad_psi[k] = 2 sum_j L_kj^*(rho_kj), rho = w - sqrt_d w/|w| (0 where w = 0, C7) (Eq. (11))
+ * grad_q_part = 2 sum_j P_{-omega_j} sum_k conj(M S psi_k) P_{-zdet_j} Z rho_kj     (Eq. (12))
+ *   (local partial: the caller allreduces it over ranks).
+ * grad_psi / grad_q_part may be NULL (not computed).  sqrt_d: float32 [K][nz][n][n] >= 0. */
+holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float *sqrt_d,
+                      const void *eta_psi_prev, void *grad_psi, void *grad_q_part, double *sc, uint32_t flags);
+
+/* Reference arm (O14; reference constraint P:102, Eq. (10)/(12) reference terms):
+ *   sc[0] = F_ref = sum_r sum_pix (|C P_{zeta0} S_{s_r} q| - sqrt_dref_r)^2
+ *   grad_q_part (+)= 2 sum_r S_{-s_r} P_{-zeta0} Z rho^r_r                       */
+holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref /*[R][n][n]*/,
+                          void *grad_q_part, double *sc, uint32_t flags);
+
+/* q-block dot products (run identically on every rank after the allreduce):
+ *   out[0] = ||grad_q||^2,  out[1] = Re<grad_q, eta_q_prev> (0 if eta_q_prev NULL).       */
+holo_status holo_q_dots(holo_plan *p, const void *grad_q, const void *eta_q_prev, double *out /*[2] device*/);
+
+/* CG step (pointwise; Eqs. (13)-(14), reading C9-C11).  in/out are [host] scalars that
+ * the caller computed after the allreduce:
+ *   if !reuse_eta:  first: eta = -P g;  else eta = -P g + beta eta,
+ *                   beta = gPg / (g_eta_prev - gprev_eta_prev);
+ *                   guard |den| < 1e-30 gPg or Re<g, eta_new> >= 0  ->  eta = -P g (reset)
+ *   x_trial = x + gamma eta          for the psi block and the q block, P = diag(rho_psi, rho_q)
+ * out->g_eta_new = Re<g, eta_new> by scalar algebra.  Any of the psi-block pointers may be
+ * NULL together (q-only CG), likewise the q-block pointers.  eta_* are updated in place.  */
+typedef struct {
+  double gPg;            /* <g, P g> = rho_psi ||g_psi||^2 + rho_q ||g_q||^2            */
+  double g_eta_prev;     /* Re<g_m, eta_{m-1}>                                          */
+  double gprev_eta_prev; /* Re<g_{m-1}, eta_{m-1}>                                      */
+  double gamma;          /* step length                                                 */
+  double rho_psi, rho_q; /* block preconditioner P                                      */
+  int32_t first;         /* 1: eta = -P g                                               */
+  int32_t reuse_eta;     /* 1: keep eta (line-search retry), only x_trial is formed     */
+} holo_cg_in;
+typedef struct {
+  double beta, g_eta_new;
+  int32_t reset;
+} holo_cg_out;
+holo_status holo_cg_step(holo_plan *p, const holo_cg_in *in /*[host]*/, holo_cg_out *out /*[host]*/,
+                         const void *psi, void *eta_psi, const void *grad_psi, void *psi_trial,
+                         const void *q, void *eta_q, const void *grad_q, void *q_trial);
+
+/* Number of kernel launches this plan has enqueued since creation (profiling aid). */
+uint64_t holo_launch_count(const holo_plan *p);
+
+/* Per-pass device timing with CUDA events recorded on the plan's stream around every
+ * launch (enable = 1 starts recording, 0 stops).  holo_profile_read synchronises on the
+ * last recorded event and returns, per pass id, the summed device time [ms], the number
+ * of launches and the ALGORITHMIC bytes / flops of those launches (DESIGN.md byte and
+ * flop model; flops use 5 L log2 L per length-L complex FFT).  Arrays are [host] of
+ * length HOLO_NPASS; any may be NULL.  reset = 1 clears the accumulators.
+ * Pass ids: */
+#define HOLO_PASS_X1 0
+#define HOLO_PASS_Y1 1
+#define HOLO_PASS_X2 2
+#define HOLO_PASS_Y2 3
+#define HOLO_PASS_X3 4
+#define HOLO_PASS_FILTER 5 /* q_j = P_omega q and g_q = 2 sum P_-omega G_j */
+#define HOLO_PASS_REDUCE 6
+#define HOLO_PASS_CG 7
+#define HOLO_PASS_REF 8
+#define HOLO_NPASS 9
+holo_status holo_profile_enable(holo_plan *p, int enable);
+holo_status holo_profile_read(holo_plan *p, double *ms, uint64_t *launches, double *bytes, double *flops, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOLO_H */

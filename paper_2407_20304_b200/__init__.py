@@ -1,0 +1,215 @@
+"""B200-native hot path of arXiv 2407.20304 (joint object/probe holotomography).
+
+Thin ctypes binding over the C ABI of ``include/holo.h`` (``libholo.so``, sm_100a):
+argument marshalling only -- every step of the path runs in the library's CUDA
+kernels.  PyTorch supplies device memory, streams and ``torch.distributed``.
+
+There is no CPU fallback: importing this package on a machine without the built
+library raises, and every call requires CUDA tensors.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+from . import _build
+
+HOLO_OK, HOLO_EINVAL, HOLO_ENOMEM, HOLO_ECUDA, HOLO_EUNSUPPORTED, HOLO_ESTATE = 0, -1, -2, -3, -4, -5
+HOLO_ACCUMULATE_Q = 1
+HOLO_OBJECTIVE_ONLY = 2
+HOLO_MAX_NZ = 8
+
+LIB_PATH = _build.LIB
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"libholo.so not found at {LIB_PATH}: build it with `python -m paper_2407_20304_b200._build` "
+        "(there is no CPU fallback)")
+_lib = ctypes.CDLL(LIB_PATH)
+
+
+class HoloGeometry(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("npad", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("n_angles", ctypes.c_int32), ("angle_batch", ctypes.c_int32),
+                ("wavelength", ctypes.c_double), ("focus_to_detector", ctypes.c_double),
+                ("z1", ctypes.c_double * HOLO_MAX_NZ), ("detector_pixel", ctypes.c_double)]
+
+
+class HoloCgIn(ctypes.Structure):
+    _fields_ = [("gPg", ctypes.c_double), ("g_eta_prev", ctypes.c_double), ("gprev_eta_prev", ctypes.c_double),
+                ("gamma", ctypes.c_double), ("rho_psi", ctypes.c_double), ("rho_q", ctypes.c_double),
+                ("first", ctypes.c_int32), ("reuse_eta", ctypes.c_int32)]
+
+
+class HoloCgOut(ctypes.Structure):
+    _fields_ = [("beta", ctypes.c_double), ("g_eta_new", ctypes.c_double), ("reset", ctypes.c_int32)]
+
+
+_P = ctypes.c_void_p
+_S = ctypes.c_int
+_lib.holo_plan_create.argtypes = [ctypes.POINTER(_P), ctypes.POINTER(HoloGeometry), ctypes.c_int, _P]
+_lib.holo_plan_create.restype = _S
+_lib.holo_plan_destroy.argtypes = [_P]
+_lib.holo_plan_destroy.restype = None
+_lib.holo_plan_workspace_bytes.argtypes = [_P]
+_lib.holo_plan_workspace_bytes.restype = ctypes.c_size_t
+_lib.holo_last_error.argtypes = [_P]
+_lib.holo_last_error.restype = ctypes.c_char_p
+_lib.holo_launch_count.argtypes = [_P]
+_lib.holo_launch_count.restype = ctypes.c_uint64
+_lib.holo_plan_derived.argtypes = [_P] + [_P] * 6
+_lib.holo_plan_derived.restype = _S
+_lib.holo_set_shifts.argtypes = [_P, _P]
+_lib.holo_set_shifts.restype = _S
+_lib.holo_set_ref_shifts.argtypes = [_P, ctypes.c_int32, _P]
+_lib.holo_set_ref_shifts.restype = _S
+_lib.holo_fwd.argtypes = [_P, _P, _P, _P]
+_lib.holo_fwd.restype = _S
+_lib.holo_adj.argtypes = [_P, _P, _P, _P, _P, _P]
+_lib.holo_adj.restype = _S
+_lib.holo_grad.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_uint32]
+_lib.holo_grad.restype = _S
+_lib.holo_grad_ref.argtypes = [_P, _P, _P, _P, _P, ctypes.c_uint32]
+_lib.holo_grad_ref.restype = _S
+_lib.holo_q_dots.argtypes = [_P, _P, _P, _P]
+_lib.holo_q_dots.restype = _S
+_lib.holo_cg_step.argtypes = [_P, ctypes.POINTER(HoloCgIn), ctypes.POINTER(HoloCgOut)] + [_P] * 8
+_lib.holo_cg_step.restype = _S
+
+EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes", "holo_last_error",
+            "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
+            "holo_grad_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count"]
+
+
+class HoloError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"holo status {status}: {msg}")
+        self.status = status
+
+
+def _ptr(t, dtype=None, numel=None, name="array"):
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name}: expected {numel} elements, got {t.numel()}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """holo_plan_create: one (device, stream) plan for K angles x nz planes on an npad^2 torus."""
+
+    def __init__(self, n, npad, z1, n_angles, wavelength, focus_to_detector, detector_pixel, device=0,
+                 stream=None, angle_batch=1):
+        g = HoloGeometry()
+        g.n, g.npad, g.nz, g.n_angles, g.angle_batch = n, npad, len(z1), n_angles, angle_batch
+        g.wavelength, g.focus_to_detector, g.detector_pixel = wavelength, focus_to_detector, detector_pixel
+        for i, z in enumerate(z1):
+            g.z1[i] = z
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        h = _P()
+        st = _lib.holo_plan_create(ctypes.byref(h), ctypes.byref(g), self.device.index or 0,
+                                   ctypes.c_void_p(stream.cuda_stream))
+        if st != HOLO_OK:
+            raise HoloError(st, "holo_plan_create failed")
+        self._h = h
+        self.n, self.npad, self.nz, self.K = n, npad, len(z1), n_angles
+        self.geometry = g
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.holo_plan_destroy(h)
+            self._h = None
+
+    def _chk(self, st):
+        if st != HOLO_OK:
+            raise HoloError(st, _lib.holo_last_error(self._h).decode())
+
+    @property
+    def workspace_bytes(self):
+        return _lib.holo_plan_workspace_bytes(self._h)
+
+    @property
+    def launch_count(self):
+        return _lib.holo_launch_count(self._h)
+
+    def derived(self):
+        nz = self.nz
+        m0, p0 = ctypes.c_double(), ctypes.c_double()
+        arrs = [(ctypes.c_double * nz)() for _ in range(4)]
+        self._chk(_lib.holo_plan_derived(self._h, ctypes.byref(m0), *[ctypes.cast(a, _P) for a in arrs],
+                                         ctypes.byref(p0)))
+        mt, zdet, omega, zeta = (np.array(a[:]) for a in arrs)
+        return dict(m0=m0.value, mt=mt, zdet=zdet, omega=omega, zeta=zeta, p0=p0.value)
+
+    def set_shifts(self, s):
+        s = np.ascontiguousarray(s, dtype=np.float64).reshape(self.K, self.nz, 2)
+        self._chk(_lib.holo_set_shifts(self._h, s.ctypes.data_as(_P)))
+
+    def set_ref_shifts(self, s):
+        s = np.ascontiguousarray(s, dtype=np.float64).reshape(-1, 2)
+        self._chk(_lib.holo_set_ref_shifts(self._h, s.shape[0], s.ctypes.data_as(_P)))
+
+    # ---- hot path
+    def fwd(self, psi, q, w):
+        LL, NN = self.npad ** 2, self.n ** 2
+        self._chk(_lib.holo_fwd(self._h, _ptr(psi, torch.complex64, self.K * LL, "psi"),
+                                _ptr(q, torch.complex64, LL, "q"),
+                                _ptr(w, torch.complex64, self.K * self.nz * NN, "w")))
+        return w
+
+    def adj(self, y, psi, q, adj_psi=None, adj_q=None):
+        LL, NN = self.npad ** 2, self.n ** 2
+        self._chk(_lib.holo_adj(self._h, _ptr(y, torch.complex64, self.K * self.nz * NN, "y"),
+                                _ptr(psi, torch.complex64, self.K * LL, "psi"), _ptr(q, torch.complex64, LL, "q"),
+                                _ptr(adj_psi, torch.complex64, self.K * LL, "adj_psi"),
+                                _ptr(adj_q, torch.complex64, LL, "adj_q")))
+
+    def grad(self, psi, q, sqrt_d, sc, eta_psi_prev=None, grad_psi=None, grad_q_part=None, flags=0):
+        LL, NN = self.npad ** 2, self.n ** 2
+        self._chk(_lib.holo_grad(self._h, _ptr(psi, torch.complex64, self.K * LL, "psi"),
+                                 _ptr(q, torch.complex64, LL, "q"),
+                                 _ptr(sqrt_d, torch.float32, self.K * self.nz * NN, "sqrt_d"),
+                                 _ptr(eta_psi_prev, torch.complex64, self.K * LL, "eta_psi_prev"),
+                                 _ptr(grad_psi, torch.complex64, self.K * LL, "grad_psi"),
+                                 _ptr(grad_q_part, torch.complex64, LL, "grad_q_part"),
+                                 _ptr(sc, torch.float64, 3, "sc"), flags))
+
+    def grad_ref(self, q, sqrt_dref, sc, grad_q_part=None, flags=0):
+        self._chk(_lib.holo_grad_ref(self._h, _ptr(q, torch.complex64, self.npad ** 2, "q"),
+                                     _ptr(sqrt_dref, torch.float32, None, "sqrt_dref"),
+                                     _ptr(grad_q_part, torch.complex64, self.npad ** 2, "grad_q_part"),
+                                     _ptr(sc, torch.float64, 1, "sc"), flags))
+
+    def q_dots(self, grad_q, eta_q_prev, out):
+        LL = self.npad ** 2
+        self._chk(_lib.holo_q_dots(self._h, _ptr(grad_q, torch.complex64, LL, "grad_q"),
+                                   _ptr(eta_q_prev, torch.complex64, LL, "eta_q_prev"),
+                                   _ptr(out, torch.float64, 2, "out")))
+
+    def cg_step(self, cin: HoloCgIn, psi=None, eta_psi=None, grad_psi=None, psi_trial=None,
+                q=None, eta_q=None, grad_q=None, q_trial=None) -> HoloCgOut:
+        out = HoloCgOut()
+        LL = self.npad ** 2
+        self._chk(_lib.holo_cg_step(self._h, ctypes.byref(cin), ctypes.byref(out),
+                                    _ptr(psi, torch.complex64, self.K * LL, "psi"),
+                                    _ptr(eta_psi, torch.complex64, self.K * LL, "eta_psi"),
+                                    _ptr(grad_psi, torch.complex64, self.K * LL, "grad_psi"),
+                                    _ptr(psi_trial, torch.complex64, self.K * LL, "psi_trial"),
+                                    _ptr(q, torch.complex64, LL, "q"), _ptr(eta_q, torch.complex64, LL, "eta_q"),
+                                    _ptr(grad_q, torch.complex64, LL, "grad_q"),
+                                    _ptr(q_trial, torch.complex64, LL, "q_trial")))
+        return out

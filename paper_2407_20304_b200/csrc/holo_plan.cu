@@ -1,0 +1,571 @@
+// holo_plan.cu -- host side of libholo: plan, fp64 table generation, argument
+// validation, pass orchestration and the C ABI of include/holo.h.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/holo.h"
+#include "holo_passes.cuh"
+
+using namespace holo;
+using cd = std::complex<double>;
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+struct Buf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct holo_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  holo_geometry g{};
+  int L = 0, N = 0, nz = 0, K = 0;
+  double m0 = 0, p0 = 0, mt[HOLO_MAX_NZ]{}, zeta[HOLO_MAX_NZ]{}, zdet[HOLO_MAX_NZ]{}, omega[HOLO_MAX_NZ]{};
+  uint32_t magmask = 0;
+  // device tables
+  float2 *tw = nullptr, *hdet = nullptr, *homega = nullptr, *cin = nullptr, *cout = nullptr, *bke = nullptr,
+         *bko = nullptr, *wodd = nullptr, *ramps = nullptr, *href = nullptr;
+  // workspace
+  float2 *T1 = nullptr, *Aw = nullptr, *W1 = nullptr, *V1 = nullptr, *T3 = nullptr, *G = nullptr, *QJ = nullptr;
+  double *partF = nullptr, *partX3 = nullptr, *partQ = nullptr;
+  size_t ws_bytes = 0;
+  std::vector<void *> allocs;
+  std::string err;
+  bool sticky = false;
+  uint64_t launches = 0;
+  int n_ref = 0;
+  std::vector<double> ref_shifts;
+
+  Tables tables() const {
+    Tables t;
+    t.tw = tw; t.hdet = hdet; t.homega = homega; t.cin = cin; t.cout = cout; t.bke = bke; t.bko = bko;
+    t.wodd = wodd; t.ramps = ramps; t.href = href;
+    return t;
+  }
+};
+
+namespace {
+
+holo_status fail(holo_plan *p, holo_status s, const std::string &msg) {
+  if (p) p->err = msg;
+  return s;
+}
+
+holo_status cuda_check(holo_plan *p, cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return HOLO_OK;
+  p->sticky = true;
+  p->err = std::string(what) + ": " + cudaGetErrorString(e);
+  return HOLO_ECUDA;
+}
+
+#define HC(call)                                                     \
+  do {                                                               \
+    holo_status _s = cuda_check(p, (call), #call);                   \
+    if (_s != HOLO_OK) return _s;                                    \
+  } while (0)
+
+template <class T>
+holo_status dalloc(holo_plan *p, T **ptr, size_t bytes) {
+  void *q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(p, HOLO_ENOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+  }
+  p->allocs.push_back(q);
+  p->ws_bytes += bytes;
+  *ptr = reinterpret_cast<T *>(q);
+  return HOLO_OK;
+}
+
+holo_status upload(holo_plan *p, float2 *dst, const std::vector<cd> &v) {
+  std::vector<float2> f(v.size());
+  for (size_t i = 0; i < v.size(); i++) f[i] = make_float2((float)v[i].real(), (float)v[i].imag());
+  HC(cudaMemcpy(dst, f.data(), f.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  return HOLO_OK;
+}
+
+long fbar(long f, long L) { return f < L / 2 ? f : f - L; }
+
+// exp(i * 2 pi * num / den) with the integer part of num/den removed in fp64
+cd expi2pi_frac(double x) {  // x in cycles
+  x -= std::floor(x);
+  return std::polar(1.0, 2.0 * kPi * x);
+}
+
+// in-place iterative radix-2 fp64 FFT (forward, unnormalised), n power of two
+void fft64(std::vector<cd> &a) {
+  const size_t n = a.size();
+  for (size_t i = 1, j = 0; i < n; i++) {
+    size_t bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+    if (i < j) std::swap(a[i], a[j]);
+  }
+  for (size_t len = 2; len <= n; len <<= 1) {
+    for (size_t i = 0; i < n; i += len)
+      for (size_t k = 0; k < len / 2; k++) {
+        cd w = std::polar(1.0, -2.0 * kPi * (double)k / (double)len);
+        cd u = a[i + k], v = a[i + k + len / 2] * w;
+        a[i + k] = u + v;
+        a[i + k + len / 2] = u - v;
+      }
+  }
+}
+
+int first_radix(int L) {  // must match FftShape<L>: S16 = (log2 L - 1) / 4, F = L / 16^S16
+  int s16 = 0, lg = 0;
+  while ((1 << lg) < L) lg++;
+  s16 = (lg - 1) / 4;
+  return L >> (4 * s16);
+}
+
+// transfer h_z[f] = exp(-i pi lambda z (fbar/(L p0))^2), phase reduced in cycles
+std::vector<cd> transfer(int L, double lam, double p0, double z) {
+  std::vector<cd> h(L);
+  for (int f = 0; f < L; f++) {
+    double fr = (double)fbar(f, L) / ((double)L * p0);
+    h[f] = expi2pi_frac(-0.5 * lam * z * fr * fr);
+  }
+  return h;
+}
+
+bool supported_L(int L) { return L == 128 || L == 256 || L == 512 || L == 1024 || L == 2048 || L == 4096; }
+
+template <int L>
+void set_smem_attrs() {
+  const int s = (int)Cfg<L>::SMEM;
+  cudaFuncSetAttribute(k_x1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_y1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_x2<L, X2_GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_x2<L, X2_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_x2<L, X2_ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_x2<L, X2_OBJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_y2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_x3<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_rows_filter<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  cudaFuncSetAttribute(k_cols_filter<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+}
+
+void set_attrs(int L) {
+  switch (L) {
+    case 128: set_smem_attrs<128>(); break;
+    case 256: set_smem_attrs<256>(); break;
+    case 512: set_smem_attrs<512>(); break;
+    case 1024: set_smem_attrs<1024>(); break;
+    case 2048: set_smem_attrs<2048>(); break;
+    case 4096: set_smem_attrs<4096>(); break;
+  }
+}
+
+// ------------------------------------------------------------------ pass runners
+template <int L>
+struct Run {
+  static constexpr size_t SM = Cfg<L>::SMEM;
+  static constexpr int NT = Cfg<L>::NT;
+
+  static void qj(holo_plan *p, const float2 *q) {
+    Tables tb = p->tables();
+    for (int j = 0; j < p->nz; j++) {
+      float2 *dst = p->QJ + (size_t)j * L * L;
+      if (p->omega[j] == 0.0) {
+        cudaMemcpyAsync(dst, q, sizeof(float2) * L * L, cudaMemcpyDeviceToDevice, p->stream);
+        continue;
+      }
+      k_rows_filter<L><<<L / 4, NT, SM, p->stream>>>(q, dst, tb, p->homega + j * L, 0, 1.0f);
+      k_cols_filter<L><<<L / 4, NT, SM, p->stream>>>(dst, dst, tb, p->homega + j * L, 0, 1.0f, 0);
+      p->launches += 2;
+    }
+  }
+
+  // g_q (+)= scale * sum_j P_{-omega_j} G_j
+  static void gq(holo_plan *p, float2 *out, float scale, bool accumulate) {
+    Tables tb = p->tables();
+    for (int j = 0; j < p->nz; j++) {
+      float2 *Gj = p->G + (size_t)j * L * L;
+      int acc = (accumulate || j > 0) ? 1 : 0;
+      if (p->omega[j] == 0.0) {
+        k_scale_add<<<1184, 256, 0, p->stream>>>(Gj, out, (size_t)L * L, scale, acc);
+        p->launches++;
+        continue;
+      }
+      k_rows_filter<L><<<L / 4, NT, SM, p->stream>>>(Gj, Gj, tb, p->homega + j * L, 1, 1.0f);
+      k_cols_filter<L><<<L / 4, NT, SM, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale, acc);
+      p->launches += 2;
+    }
+  }
+
+  // mode: 0 grad, 1 fwd, 2 adj (y given), 3 objective only
+  static void sweep(holo_plan *p, int mode, const float2 *psi, const float2 *q, const float *sqrt_d,
+                    const float2 *yin, float2 *wout, const float2 *eta, float2 *gpsi, float2 *gq_out, float gscale,
+                    bool want_q) {
+    Tables tb = p->tables();
+    const int N = p->N, nz = p->nz, K = p->K;
+    const size_t LL = (size_t)L * L;
+    const int nbx2 = (N + 3) / 4;
+    qj(p, q);
+    if (want_q) cudaMemsetAsync(p->G, 0, sizeof(float2) * LL * nz, p->stream);
+    for (int k = 0; k < K; k++) {
+      const float2 *psik = psi + (size_t)k * LL;
+      const bool need_fwd_chain = (mode != 2) || want_q;
+      if (need_fwd_chain) {
+        k_x1<L><<<L / 2, NT, SM, p->stream>>>(psik, p->T1, tb, k, nz, p->magmask);
+        p->launches++;
+      }
+      for (int j = 0; j < nz; j++) {
+        const int mag = (p->magmask >> j) & 1;
+        const float2 *T1j = p->T1 + (size_t)j * LL;
+        const float2 *qjj = p->QJ + (size_t)j * LL;
+        const size_t fr = (size_t)k * nz + j;
+        if (need_fwd_chain) {
+          float2 *aout = want_q ? p->Aw : nullptr;
+          float2 *w1 = (mode == 2) ? nullptr : p->W1;
+          k_y1<L><<<L / 4, NT, SM, p->stream>>>(T1j, qjj, aout, w1, tb, k, j, nz, mag, N);
+          p->launches++;
+        }
+        double *pf = p->partF + fr * nbx2;
+        if (mode == 1) {
+          k_x2<L, X2_FWD><<<nbx2, NT, SM, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, j, N);
+          p->launches++;
+          continue;
+        }
+        if (mode == 3) {
+          k_x2<L, X2_OBJ><<<nbx2, NT, SM, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, j, N);
+          p->launches++;
+          continue;
+        }
+        if (mode == 0)
+          k_x2<L, X2_GRAD><<<nbx2, NT, SM, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, j, N);
+        else
+          k_x2<L, X2_ADJ><<<nbx2, NT, SM, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, j, N);
+        k_y2<L><<<L / 4, NT, SM, p->stream>>>(p->V1, p->Aw, qjj, want_q ? p->G + (size_t)j * LL : nullptr,
+                                               gpsi ? p->T3 + (size_t)j * LL : nullptr, tb, k, j, nz, mag, N);
+        p->launches += 2;
+      }
+      if (gpsi && (mode == 0 || mode == 2)) {
+        k_x3<L><<<L / 2, NT, SM, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
+                                               p->partX3 + (size_t)k * L, tb, k, nz, p->magmask, gscale);
+        p->launches++;
+      }
+    }
+    if (want_q && (mode == 0 || mode == 2)) gq(p, gq_out, gscale, false);
+  }
+};
+
+template <template <int> class R, class... A>
+void dispatch_sweep(holo_plan *p, A... a) {
+  switch (p->L) {
+    case 128: R<128>::sweep(p, a...); break;
+    case 256: R<256>::sweep(p, a...); break;
+    case 512: R<512>::sweep(p, a...); break;
+    case 1024: R<1024>::sweep(p, a...); break;
+    case 2048: R<2048>::sweep(p, a...); break;
+    case 4096: R<4096>::sweep(p, a...); break;
+  }
+}
+
+holo_status precheck(holo_plan *p) {
+  if (!p) return HOLO_EINVAL;
+  if (p->sticky) return fail(p, HOLO_ESTATE, "plan is in an error state: " + p->err);
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return cuda_check(p, e, "cudaSetDevice");
+  return HOLO_OK;
+}
+
+holo_status postcheck(holo_plan *p) { return cuda_check(p, cudaGetLastError(), "kernel launch"); }
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device, void *stream) {
+  if (!out || !g) return HOLO_EINVAL;
+  *out = nullptr;
+  const int L = g->npad, N = g->n, nz = g->nz, K = g->n_angles;
+  if (nz < 1 || nz > HOLO_MAX_NZ || N < 8 || N % 2 || N > L || (L - N) % 2 || K < 0) return HOLO_EINVAL;
+  if (!(g->wavelength > 0) || !(g->detector_pixel > 0) || !(g->focus_to_detector > 0) || !std::isfinite(g->wavelength))
+    return HOLO_EINVAL;
+  for (int j = 0; j < nz; j++) {
+    if (!(g->z1[j] > 0) || !(g->z1[j] < g->focus_to_detector)) return HOLO_EINVAL;
+    if (j > 0 && !(g->z1[j] > g->z1[j - 1])) return HOLO_EINVAL;
+  }
+  if (L < 16 || (L & (L - 1))) return HOLO_EUNSUPPORTED;
+  if (!supported_L(L)) return HOLO_EUNSUPPORTED;
+  if (N % 4) return HOLO_EUNSUPPORTED;  // float4 row I/O of N-wide frames
+  holo_plan *p = new holo_plan();
+  p->device = device;
+  p->stream = reinterpret_cast<cudaStream_t>(stream);
+  p->g = *g;
+  p->L = L; p->N = N; p->nz = nz; p->K = K;
+  // ---- O1 geometry (Eq. (8))
+  const double Z = g->focus_to_detector;
+  p->m0 = Z / g->z1[0];
+  p->p0 = g->detector_pixel / p->m0;
+  for (int j = 0; j < nz; j++) {
+    p->mt[j] = g->z1[j] / g->z1[0];
+    p->zeta[j] = g->z1[j] * (Z - g->z1[j]) / Z;
+    p->omega[j] = (g->z1[j] - g->z1[0]) / p->mt[j];
+    p->zdet[j] = p->zeta[j] / (p->mt[j] * p->mt[j]);
+    if (p->mt[j] != 1.0) p->magmask |= 1u << j;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) { delete p; return HOLO_ECUDA; }
+  set_attrs(L);
+  holo_status s = HOLO_OK;
+  const size_t LL = (size_t)L * L;
+  auto A = [&](auto **ptr, size_t bytes) { if (s == HOLO_OK) s = dalloc(p, ptr, bytes); };
+  A(&p->tw, sizeof(float2) * L);
+  A(&p->hdet, sizeof(float2) * L * nz);
+  A(&p->homega, sizeof(float2) * L * nz);
+  A(&p->cin, sizeof(float2) * L * nz);
+  A(&p->cout, sizeof(float2) * L * nz);
+  A(&p->bke, sizeof(float2) * L * nz);
+  A(&p->bko, sizeof(float2) * L * nz);
+  A(&p->wodd, sizeof(float2) * L);
+  A(&p->href, sizeof(float2) * L);
+  A(&p->ramps, sizeof(float2) * L * 2 * nz * (size_t)(K > 0 ? K : 1));
+  A(&p->T1, sizeof(float2) * LL * nz);
+  A(&p->Aw, sizeof(float2) * LL);
+  A(&p->W1, sizeof(float2) * (size_t)N * L);
+  A(&p->V1, sizeof(float2) * (size_t)N * L);
+  A(&p->T3, sizeof(float2) * LL * nz);
+  A(&p->G, sizeof(float2) * LL * nz);
+  A(&p->QJ, sizeof(float2) * LL * nz);
+  A(&p->partF, sizeof(double) * (size_t)(K > 0 ? K : 1) * nz * ((N + 3) / 4));
+  A(&p->partX3, sizeof(double) * (size_t)(K > 0 ? K : 1) * L);
+  A(&p->partQ, sizeof(double) * 2 * 1184);
+  if (s != HOLO_OK) { holo_plan_destroy(p); return s; }
+  // ---- tables (fp64 -> fp32)
+  {
+    const int F = first_radix(L);
+    std::vector<cd> tw;
+    for (int Ns = F; Ns < L; Ns *= 16)
+      for (int r = 1; r < 16; r++)
+        for (int m = 0; m < Ns; m++) tw.push_back(expi2pi_frac(-(double)(m * r) / (16.0 * Ns)));
+    tw.resize(L, cd(0, 0));
+    if (s == HOLO_OK) s = upload(p, p->tw, tw);
+    std::vector<cd> hd, ho, ci, co, be, bo;
+    for (int j = 0; j < nz; j++) {
+      auto h1 = transfer(L, g->wavelength, p->p0, p->zdet[j]);
+      auto h2 = transfer(L, g->wavelength, p->p0, p->omega[j]);
+      hd.insert(hd.end(), h1.begin(), h1.end());
+      ho.insert(ho.end(), h2.begin(), h2.end());
+      const double mt = p->mt[j];
+      // cin[f] = kappa (-1)^fbar e^{i pi mt fbar^2 / L} / L ; phase in cycles: mt fbar^2 / (2L)
+      for (int f = 0; f < L; f++) {
+        long fb = fbar(f, L);
+        double v = mt * (double)fb;
+        bool kap = v >= -(double)(L / 2) && v < (double)(L / 2);
+        double cyc = std::fmod(mt * (double)(fb * fb), 2.0 * L) / (2.0 * L) + (fb & 1 ? 0.5 : 0.0);
+        ci.push_back(kap ? expi2pi_frac(cyc) / (double)L : cd(0, 0));
+      }
+      for (int o = 0; o < L; o++) {
+        long n = o - L / 2;
+        co.push_back(expi2pi_frac(std::fmod(mt * (double)(n * n), 2.0 * L) / (2.0 * L)));
+      }
+      // b[d] = exp(-i pi mt d^2 / L), |d| < L, on a 2L cycle; Bhat = FFT_2L(b) / (2L)
+      std::vector<cd> b(2 * L, cd(0, 0));
+      for (int d = 0; d < L; d++) {
+        cd v = expi2pi_frac(-std::fmod(mt * (double)((long)d * d), 2.0 * L) / (2.0 * L));
+        b[d] = v;
+        if (d > 0) b[2 * L - d] = v;
+      }
+      fft64(b);
+      for (int kk = 0; kk < L; kk++) {
+        be.push_back(b[2 * kk] / (2.0 * L));
+        bo.push_back(b[2 * kk + 1] / (2.0 * L));
+      }
+    }
+    if (s == HOLO_OK) s = upload(p, p->hdet, hd);
+    if (s == HOLO_OK) s = upload(p, p->homega, ho);
+    if (s == HOLO_OK) s = upload(p, p->cin, ci);
+    if (s == HOLO_OK) s = upload(p, p->cout, co);
+    if (s == HOLO_OK) s = upload(p, p->bke, be);
+    if (s == HOLO_OK) s = upload(p, p->bko, bo);
+    std::vector<cd> wo(L);
+    for (int i = 0; i < L; i++) wo[i] = expi2pi_frac(-(double)i / (2.0 * L));
+    if (s == HOLO_OK) s = upload(p, p->wodd, wo);
+    if (s == HOLO_OK) s = upload(p, p->href, transfer(L, g->wavelength, p->p0, p->zeta[0]));
+    std::vector<cd> one((size_t)L * 2 * nz * (K > 0 ? K : 1), cd(1, 0));
+    if (s == HOLO_OK) s = upload(p, p->ramps, one);
+  }
+  if (s != HOLO_OK) { holo_plan_destroy(p); return s; }
+  *out = p;
+  return HOLO_OK;
+}
+
+void holo_plan_destroy(holo_plan *p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  for (void *a : p->allocs) cudaFree(a);
+  delete p;
+}
+
+size_t holo_plan_workspace_bytes(const holo_plan *p) { return p ? p->ws_bytes : 0; }
+
+const char *holo_last_error(const holo_plan *p) { return p ? p->err.c_str() : "null plan"; }
+
+uint64_t holo_launch_count(const holo_plan *p) { return p ? p->launches : 0; }
+
+holo_status holo_plan_derived(const holo_plan *p, double *m0, double *mt, double *zdet, double *omega, double *zeta,
+                              double *p0) {
+  if (!p) return HOLO_EINVAL;
+  if (m0) *m0 = p->m0;
+  if (p0) *p0 = p->p0;
+  for (int j = 0; j < p->nz; j++) {
+    if (mt) mt[j] = p->mt[j];
+    if (zdet) zdet[j] = p->zdet[j];
+    if (omega) omega[j] = p->omega[j];
+    if (zeta) zeta[j] = p->zeta[j];
+  }
+  return HOLO_OK;
+}
+
+holo_status holo_set_shifts(holo_plan *p, const double *s) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!s) return fail(p, HOLO_EINVAL, "null shifts");
+  const int L = p->L, nz = p->nz, K = p->K;
+  for (size_t i = 0; i < (size_t)K * nz * 2; i++)
+    if (!std::isfinite(s[i]) || std::fabs(s[i]) >= L / 2) return fail(p, HOLO_EINVAL, "shift not finite or >= npad/2");
+  std::vector<float2> r((size_t)K * nz * 2 * L);
+  for (int k = 0; k < K; k++)
+    for (int j = 0; j < nz; j++)
+      for (int ax = 0; ax < 2; ax++) {
+        const double sv = s[((size_t)k * nz + j) * 2 + ax];
+        float2 *dst = r.data() + (((size_t)k * nz + j) * 2 + ax) * L;
+        for (int f = 0; f < L; f++) {
+          cd v = expi2pi_frac(-(double)fbar(f, L) * sv / (double)L);  // r_s[f] = e^{-2 pi i fbar s / L}
+          dst[f] = make_float2((float)v.real(), (float)v.imag());
+        }
+      }
+  HC(cudaMemcpy(p->ramps, r.data(), r.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  return HOLO_OK;
+}
+
+holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (n_ref < 0 || (n_ref > 0 && !s)) return fail(p, HOLO_EINVAL, "bad reference shifts");
+  for (int i = 0; i < 2 * n_ref; i++)
+    if (!std::isfinite(s[i]) || std::fabs(s[i]) >= p->L / 2) return fail(p, HOLO_EINVAL, "shift not finite or >= npad/2");
+  p->n_ref = n_ref;
+  p->ref_shifts.assign(s, s + 2 * n_ref);
+  return HOLO_OK;
+}
+
+holo_status holo_fwd(holo_plan *p, const void *psi, const void *q, void *w) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!psi || !q || !w) return fail(p, HOLO_EINVAL, "null pointer");
+  dispatch_sweep<Run>(p, 1, (const float2 *)psi, (const float2 *)q, (const float *)nullptr, (const float2 *)nullptr,
+                      (float2 *)w, (const float2 *)nullptr, (float2 *)nullptr, (float2 *)nullptr, 1.0f, false);
+  return postcheck(p);
+}
+
+holo_status holo_adj(holo_plan *p, const void *y, const void *psi, const void *q, void *adj_psi, void *adj_q) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!y || !psi || !q) return fail(p, HOLO_EINVAL, "null pointer");
+  if (!adj_psi && !adj_q) return HOLO_OK;
+  dispatch_sweep<Run>(p, 2, (const float2 *)psi, (const float2 *)q, (const float *)nullptr, (const float2 *)y,
+                      (float2 *)nullptr, (const float2 *)nullptr, (float2 *)adj_psi, (float2 *)adj_q, 1.0f,
+                      adj_q != nullptr);
+  return postcheck(p);
+}
+
+holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float *sqrt_d, const void *eta_psi_prev,
+                      void *grad_psi, void *grad_q_part, double *sc, uint32_t flags) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!psi || !q || !sqrt_d || !sc) return fail(p, HOLO_EINVAL, "null pointer");
+  if (flags & HOLO_ACCUMULATE_Q) return fail(p, HOLO_EUNSUPPORTED, "HOLO_ACCUMULATE_Q not implemented for holo_grad");
+  const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0;
+  const int K = p->K, nz = p->nz, N = p->N, L = p->L;
+  HC(cudaMemsetAsync(sc, 0, 3 * sizeof(double), p->stream));
+  if (K == 0) return HOLO_OK;
+  dispatch_sweep<Run>(p, obj ? 3 : 0, (const float2 *)psi, (const float2 *)q, sqrt_d, (const float2 *)nullptr,
+                      (float2 *)nullptr, (const float2 *)eta_psi_prev, obj ? nullptr : (float2 *)grad_psi,
+                      obj ? nullptr : (float2 *)grad_q_part, 2.0f, !obj && grad_q_part != nullptr);
+  k_reduce<<<1, 1024, 0, p->stream>>>(p->partF, (size_t)K * nz * ((N + 3) / 4), 1, sc, 0);
+  p->launches++;
+  if (!obj && grad_psi) {
+    k_reduce<<<1, 1024, 0, p->stream>>>(p->partX3, (size_t)K * (L / 2), 2, sc + 1, 0);
+    p->launches++;
+  }
+  return postcheck(p);
+}
+
+holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref, void *grad_q_part, double *sc,
+                          uint32_t flags) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  (void)q; (void)sqrt_dref; (void)grad_q_part; (void)sc; (void)flags;
+  return fail(p, HOLO_EUNSUPPORTED, "holo_grad_ref: reference arm not built yet");
+}
+
+holo_status holo_q_dots(holo_plan *p, const void *grad_q, const void *eta_q_prev, double *out) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!grad_q || !out) return fail(p, HOLO_EINVAL, "null pointer");
+  const size_t n = (size_t)p->L * p->L;
+  k_dots<<<1184, 256, 0, p->stream>>>((const float2 *)grad_q, (const float2 *)eta_q_prev, n, p->partQ);
+  k_reduce<<<1, 1024, 0, p->stream>>>(p->partQ, 1184, 2, out, 0);
+  p->launches += 2;
+  return postcheck(p);
+}
+
+holo_status holo_cg_step(holo_plan *p, const holo_cg_in *in, holo_cg_out *out, const void *psi, void *eta_psi,
+                         const void *grad_psi, void *psi_trial, const void *q, void *eta_q, const void *grad_q,
+                         void *q_trial) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!in || !out) return fail(p, HOLO_EINVAL, "null pointer");
+  if (!std::isfinite(in->gamma) || !std::isfinite(in->gPg)) return fail(p, HOLO_EINVAL, "non-finite CG scalar");
+  int mode = 2;
+  double beta = 0.0, gen = in->g_eta_prev;  // for reuse_eta the caller tracks its own scalars
+  int reset = 0;
+  if (!in->reuse_eta) {
+    if (in->first) {
+      mode = 0; reset = 1; gen = -in->gPg;
+    } else {
+      double den = in->g_eta_prev - in->gprev_eta_prev;
+      if (!(std::fabs(den) >= 1e-30 * in->gPg)) {
+        mode = 0; reset = 1; gen = -in->gPg;
+      } else {
+        beta = in->gPg / den;
+        gen = -in->gPg + beta * in->g_eta_prev;  // Re<g, -P g + beta eta_prev>
+        if (!(gen < 0.0)) { mode = 0; reset = 1; beta = 0.0; gen = -in->gPg; } else mode = 1;
+      }
+    }
+  }
+  out->beta = beta;
+  out->g_eta_new = gen;
+  out->reset = reset;
+  const size_t LL = (size_t)p->L * p->L;
+  if (psi && eta_psi && psi_trial && (grad_psi || mode == 2)) {
+    k_cg<<<1184, 256, 0, p->stream>>>((const float4 *)psi, (float4 *)eta_psi, (const float4 *)grad_psi,
+                                      (float4 *)psi_trial, LL * p->K / 2, (float)in->rho_psi, (float)beta,
+                                      (float)in->gamma, mode);
+    p->launches++;
+  }
+  if (q && eta_q && q_trial && (grad_q || mode == 2)) {
+    k_cg<<<1184, 256, 0, p->stream>>>((const float4 *)q, (float4 *)eta_q, (const float4 *)grad_q, (float4 *)q_trial,
+                                      LL / 2, (float)in->rho_q, (float)beta, (float)in->gamma, mode);
+    p->launches++;
+  }
+  return postcheck(p);
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+"""GPU (sm_100a, libholo.so through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerances (BASELINE.json north_star): relative L2 error <= 2e-5 on the forward data,
+<= 1e-4 on the gradients; F and the DY scalars <= 1e-4 relative (SURVEY 8c protocol).
+Parity states are non-converged (|| |w| - sqrt d || / || sqrt d || >= 0.05).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import np_oracle as npo
+
+pytestmark = pytest.mark.gpu
+
+TOL_W, TOL_G, TOL_S = 2e-5, 1e-4, 1e-4
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+
+
+def geom(cfg, z1=None):
+    return oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1 if z1 is None else z1, cfg.det_pixel)
+
+
+def make_plan(cfg, K, L=None, N=None, z1=None):
+    import paper_2407_20304_b200 as hb
+    z1 = cfg.z1 if z1 is None else z1
+    return hb.Plan(cfg.n if N is None else N, cfg.npad if L is None else L, z1, K, cfg.wavelength, cfg.Z,
+                   cfg.det_pixel, device=0)
+
+
+def dev(x, dt=torch.complex64):
+    return torch.as_tensor(np.ascontiguousarray(x)).to(dt).cuda().contiguous()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().astype(np.complex128 if t.is_complex() else np.float64)
+
+
+class Case:
+    """Truth from synth, data from the ORACLE forward (never from the GPU), and a
+    non-converged evaluation state (psi = 1, q = 0.9 q_truth)."""
+
+    def __init__(self, name, K, oracle_kind="c", noise=True):
+        cfg = synth.CONFIGS[name]
+        self.cfg, self.K = cfg, K
+        self.g = geom(cfg)
+        self.psi_t = synth.psi_stack(cfg, K=K).numpy()
+        self.q_t = synth.probe(cfg).numpy()
+        self.s = synth.shifts(cfg, K=K)
+        L, N = cfg.npad, cfg.n
+        if oracle_kind == "c":
+            w = oracle.fwd(self.g, self.psi_t, self.q_t, self.s, N)
+        else:
+            pr = npo.Problem(self.g, L, N)
+            out = pr.fwd(self.psi_t, self.q_t, self.s)
+            w = np.stack([np.stack([out[(k, j)] for j in range(cfg.nz)]) for k in range(K)])
+        self.w = w
+        self.d = synth.poisson_amplitude(np.abs(w) ** 2, cfg.photons, cfg) if noise else np.abs(w)
+        self.psi = np.ones_like(self.psi_t)
+        self.q = 0.9 * self.q_t
+        self.kind = oracle_kind
+
+    def oracle_grad(self):
+        if self.kind == "c":
+            return oracle.grad(self.g, self.psi, self.q, self.s, self.d)
+        return npo.Problem(self.g, self.cfg.npad, self.cfg.n).grad(self.psi, self.q, self.s, self.d)
+
+
+@pytest.fixture(scope="module")
+def cfg0():
+    return Case("cfg0", 4)
+
+
+def test_library_loads_and_plan(cfg0):
+    p = make_plan(cfg0.cfg, cfg0.K)
+    d = p.derived()
+    assert np.allclose(d["mt"], cfg0.g.mt, rtol=1e-15) and np.allclose(d["zdet"], cfg0.g.zdet, rtol=1e-15)
+    assert np.allclose(d["omega"], cfg0.g.omega, rtol=1e-15) and abs(d["p0"] - cfg0.g.p0) < 1e-22
+    assert p.workspace_bytes > 0
+
+
+def test_cfg0_forward_parity(cfg0):
+    c = cfg0
+    p = make_plan(c.cfg, c.K)
+    p.set_shifts(c.s)
+    w = torch.empty(c.K, c.cfg.nz, c.cfg.n, c.cfg.n, dtype=torch.complex64, device="cuda")
+    p.fwd(dev(c.psi_t), dev(c.q_t), w)
+    wo = oracle.fwd(c.g, c.psi_t, c.q_t, c.s, c.cfg.n)
+    assert rel(host(w), wo) < TOL_W
+
+
+def test_cfg0_gradient_parity(cfg0):
+    c = cfg0
+    p = make_plan(c.cfg, c.K)
+    p.set_shifts(c.s)
+    F, gp, gq = c.oracle_grad()
+    assert np.linalg.norm(np.abs(oracle.fwd(c.g, c.psi, c.q, c.s, c.cfg.n)) - c.d) / np.linalg.norm(c.d) > 0.05
+    eta = (np.random.default_rng(1).standard_normal(c.psi.shape) * (1 + 1j)).astype(np.complex64)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, dev(eta), gpsi, gqd)
+    s = host(sc).real
+    assert abs(s[0] - F) / F < TOL_S
+    assert rel(host(gpsi), gp) < TOL_G
+    assert rel(host(gqd), gq) < TOL_G
+    assert abs(s[1] - np.vdot(gp, gp).real) / np.vdot(gp, gp).real < TOL_S
+    ge = np.vdot(eta, gp).real
+    assert abs(s[2] - ge) / abs(ge) < 1e-3  # Re<g, eta> of random eta is a cancelling sum
+
+
+def test_cfg0_objective_only_matches(cfg0):
+    c = cfg0
+    p = make_plan(c.cfg, c.K)
+    p.set_shifts(c.s)
+    import paper_2407_20304_b200 as hb
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, flags=hb.HOLO_OBJECTIVE_ONLY)
+    F = oracle.grad(c.g, c.psi, c.q, c.s, c.d, False, False)[0]
+    assert abs(host(sc).real[0] - F) / F < TOL_S
+
+
+def test_cfg0_adjoint_parity(cfg0):
+    c = cfg0
+    p = make_plan(c.cfg, c.K)
+    p.set_shifts(c.s)
+    rng = np.random.default_rng(5)
+    y = rng.standard_normal((c.K, c.cfg.nz, c.cfg.n, c.cfg.n)) + 1j * rng.standard_normal((c.K, c.cfg.nz, c.cfg.n, c.cfg.n))
+    ap, aq = oracle.adj(c.g, y, c.psi_t, c.q_t, c.s)
+    gap = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
+    gaq = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
+    p.adj(dev(y), dev(c.psi_t), dev(c.q_t), gap, gaq)
+    assert rel(host(gap), ap) < TOL_G and rel(host(gaq), aq) < TOL_G
+
+
+def test_cfg1_parity_two_angles():
+    c = Case("cfg1", 2, oracle_kind="np")
+    p = make_plan(c.cfg, c.K)
+    p.set_shifts(c.s)
+    w = torch.empty(c.K, c.cfg.nz, c.cfg.n, c.cfg.n, dtype=torch.complex64, device="cuda")
+    p.fwd(dev(c.psi_t), dev(c.q_t), w)
+    pr = npo.Problem(c.g, c.cfg.npad, c.cfg.n)
+    out = pr.fwd(c.psi_t, c.q_t, c.s)
+    wn = host(w)
+    for (k, j), wo in out.items():
+        assert rel(wn[k, j], wo) < TOL_W, (k, j)
+    F, gp, gq = c.oracle_grad()
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, gpsi, gqd)
+    assert abs(host(sc).real[0] - F) / F < TOL_S
+    assert rel(host(gpsi), gp) < TOL_G and rel(host(gqd), gq) < TOL_G
+
+
+@pytest.mark.parametrize("L", [256, 1024])
+def test_other_torus_sizes_forward(L):
+    """FFT shapes F = 16 (L = 256) and F = 4 (L = 1024), random psi/q, ragged shifts."""
+    cfg = synth.CONFIGS["cfg1"]
+    N = L // 2
+    rng = np.random.default_rng(L)
+    K = 1
+    psi = 1 + 0.3 * (rng.standard_normal((K, L, L)) + 1j * rng.standard_normal((K, L, L)))
+    q = 1 + 0.3 * (rng.standard_normal((L, L)) + 1j * rng.standard_normal((L, L)))
+    s = rng.uniform(-3, 3, size=(K, cfg.nz, 2))
+    g = geom(cfg)
+    p = make_plan(cfg, K, L=L, N=N)
+    p.set_shifts(s)
+    w = torch.empty(K, cfg.nz, N, N, dtype=torch.complex64, device="cuda")
+    p.fwd(dev(psi), dev(q), w)
+    out = npo.Problem(g, L, N).fwd(psi, q, s)
+    wn = host(w)
+    for (k, j), wo in out.items():
+        assert rel(wn[k, j], wo) < TOL_W, (k, j)
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_full_size_one_angle_parity(name):
+    """Full torus sizes (2048^2, 4096^2) in the bench's launch configuration, one angle x 4 planes."""
+    c = Case(name, 1, oracle_kind="np", noise=False)
+    p = make_plan(c.cfg, 1)
+    p.set_shifts(c.s)
+    w = torch.empty(1, c.cfg.nz, c.cfg.n, c.cfg.n, dtype=torch.complex64, device="cuda")
+    p.fwd(dev(c.psi_t), dev(c.q_t), w)
+    wn = host(w)
+    for j in range(c.cfg.nz):
+        assert rel(wn[0, j], c.w[0, j]) < TOL_W, j
+    F, gp, gq = c.oracle_grad()
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, gpsi, gqd)
+    assert abs(host(sc).real[0] - F) / F < TOL_S
+    assert rel(host(gpsi), gp) < TOL_G and rel(host(gqd), gq) < TOL_G
