@@ -25,7 +25,7 @@ HOLO_MAX_NZ = 8
 LIB_PATH = _build.LIB
 if not os.path.exists(LIB_PATH):
     raise ImportError(
-        f"libholo.so not found at {LIB_PATH}: build it with `python -m paper_2407_20304_b200._build` "
+        f"libholo.so not found at {LIB_PATH}: build it with `python paper_2407_20304_b200/_build.py` "
         "(there is no CPU fallback)")
 _lib = ctypes.CDLL(LIB_PATH)
 
@@ -78,9 +78,20 @@ _lib.holo_q_dots.restype = _S
 _lib.holo_cg_step.argtypes = [_P, ctypes.POINTER(HoloCgIn), ctypes.POINTER(HoloCgOut)] + [_P] * 8
 _lib.holo_cg_step.restype = _S
 
+_lib.holo_profile_enable.argtypes = [_P, ctypes.c_int]
+_lib.holo_profile_enable.restype = _S
+_lib.holo_profile_read.argtypes = [_P, _P, _P, _P, _P, ctypes.c_int]
+_lib.holo_profile_read.restype = _S
+
+HOLO_NPASS = 9
+PASS_NAMES = ["X1", "Y1", "X2", "Y2", "X3", "filter", "reduce", "cg", "ref"]
+PASS_KERNELS = ["k_x1", "k_y1", "k_x2", "k_y2", "k_x3", "k_rows_filter|k_cols_filter|k_scale_add",
+                "k_reduce|k_dots", "k_cg", "k_ref"]
+
 EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes", "holo_last_error",
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
-            "holo_grad_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count"]
+            "holo_grad_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
+            "holo_profile_read"]
 
 
 class HoloError(RuntimeError):
@@ -145,6 +156,19 @@ class Plan:
     @property
     def launch_count(self):
         return _lib.holo_launch_count(self._h)
+
+    def profile_enable(self, on=True):
+        self._chk(_lib.holo_profile_enable(self._h, int(bool(on))))
+
+    def profile_read(self, reset=True):
+        """Per-pass {name: dict(ms, launches, bytes, flops)} from CUDA events on the plan's stream."""
+        ms = (ctypes.c_double * HOLO_NPASS)()
+        n = (ctypes.c_uint64 * HOLO_NPASS)()
+        b = (ctypes.c_double * HOLO_NPASS)()
+        f = (ctypes.c_double * HOLO_NPASS)()
+        self._chk(_lib.holo_profile_read(self._h, ctypes.cast(ms, _P), ctypes.cast(n, _P), ctypes.cast(b, _P),
+                                         ctypes.cast(f, _P), int(bool(reset))))
+        return {PASS_NAMES[i]: dict(ms=ms[i], launches=n[i], bytes=b[i], flops=f[i]) for i in range(HOLO_NPASS)}
 
     def derived(self):
         nz = self.nz

@@ -46,6 +46,14 @@ struct holo_plan {
   uint64_t launches = 0;
   int n_ref = 0;
   std::vector<double> ref_shifts;
+  // per-pass event profiling (holo_profile_*)
+  struct Rec { int id; double bytes, flops; size_t ev; };
+  bool prof_on = false;
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  std::vector<Rec> recs;
+  double pms[HOLO_NPASS]{}, pbytes[HOLO_NPASS]{}, pflops[HOLO_NPASS]{};
+  uint64_t pcnt[HOLO_NPASS]{};
 
   Tables tables() const {
     Tables t;
@@ -169,40 +177,90 @@ void set_attrs(int L) {
   }
 }
 
+// ------------------------------------------------------------------ profiling
+void prof_flush(holo_plan *p) {
+  if (p->recs.empty()) return;
+  cudaEventSynchronize(p->evpool[p->recs.back().ev + 1]);
+  for (const auto &r : p->recs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p->evpool[r.ev], p->evpool[r.ev + 1]);
+    p->pms[r.id] += ms;
+    p->pbytes[r.id] += r.bytes;
+    p->pflops[r.id] += r.flops;
+    p->pcnt[r.id]++;
+  }
+  p->recs.clear();
+  p->evused = 0;
+}
+
+void pbeg(holo_plan *p) {
+  if (!p->prof_on) return;
+  if (p->evused + 2 > 32768) prof_flush(p);
+  while (p->evpool.size() < p->evused + 2) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    p->evpool.push_back(e);
+  }
+  cudaEventRecord(p->evpool[p->evused], p->stream);
+}
+
+void pend(holo_plan *p, int id, double bytes, double flops) {
+  p->launches++;
+  if (!p->prof_on) return;
+  cudaEventRecord(p->evpool[p->evused + 1], p->stream);
+  p->recs.push_back({id, bytes, flops, p->evused});
+  p->evused += 2;
+}
+
+double fftf(int L) {  // 5 L log2 L flops per length-L complex FFT
+  int lg = 0;
+  while ((1 << lg) < L) lg++;
+  return 5.0 * L * lg;
+}
+
 // ------------------------------------------------------------------ pass runners
 template <int L>
 struct Run {
   static constexpr size_t SM = Cfg<L>::SMEM;
   static constexpr int NT = Cfg<L>::NT;
+  static constexpr double A = 8.0 * L * L;  // bytes of one L x L complex64 array
+
+  static void rows_filter(holo_plan *p, const float2 *in, float2 *out, const float2 *h, int conj, float scale) {
+    pbeg(p);
+    k_rows_filter<L><<<L / 4, NT, SM, p->stream>>>(in, out, p->tables(), h, conj, scale);
+    pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
+  }
+  static void cols_filter(holo_plan *p, const float2 *in, float2 *out, const float2 *h, int conj, float scale, int acc) {
+    pbeg(p);
+    k_cols_filter<L><<<L / 4, NT, SM, p->stream>>>(in, out, p->tables(), h, conj, scale, acc);
+    pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 2.0 * L * fftf(L));
+  }
 
   static void qj(holo_plan *p, const float2 *q) {
-    Tables tb = p->tables();
     for (int j = 0; j < p->nz; j++) {
       float2 *dst = p->QJ + (size_t)j * L * L;
       if (p->omega[j] == 0.0) {
         cudaMemcpyAsync(dst, q, sizeof(float2) * L * L, cudaMemcpyDeviceToDevice, p->stream);
         continue;
       }
-      k_rows_filter<L><<<L / 4, NT, SM, p->stream>>>(q, dst, tb, p->homega + j * L, 0, 1.0f);
-      k_cols_filter<L><<<L / 4, NT, SM, p->stream>>>(dst, dst, tb, p->homega + j * L, 0, 1.0f, 0);
-      p->launches += 2;
+      rows_filter(p, q, dst, p->homega + j * L, 0, 1.0f);
+      cols_filter(p, dst, dst, p->homega + j * L, 0, 1.0f, 0);
     }
   }
 
   // g_q (+)= scale * sum_j P_{-omega_j} G_j
   static void gq(holo_plan *p, float2 *out, float scale, bool accumulate) {
-    Tables tb = p->tables();
     for (int j = 0; j < p->nz; j++) {
       float2 *Gj = p->G + (size_t)j * L * L;
       int acc = (accumulate || j > 0) ? 1 : 0;
       if (p->omega[j] == 0.0) {
+        pbeg(p);
         k_scale_add<<<1184, 256, 0, p->stream>>>(Gj, out, (size_t)L * L, scale, acc);
-        p->launches++;
+        pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 0);
         continue;
       }
-      k_rows_filter<L><<<L / 4, NT, SM, p->stream>>>(Gj, Gj, tb, p->homega + j * L, 1, 1.0f);
-      k_cols_filter<L><<<L / 4, NT, SM, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale, acc);
-      p->launches += 2;
+      rows_filter(p, Gj, Gj, p->homega + j * L, 1, 1.0f);
+      cols_filter(p, Gj, out, p->homega + j * L, 1, scale, acc);
     }
   }
 
@@ -214,14 +272,18 @@ struct Run {
     const int N = p->N, nz = p->nz, K = p->K;
     const size_t LL = (size_t)L * L;
     const int nbx2 = (N + 3) / 4;
+    const double fl = fftf(L), rN = (double)N / L, NN8 = 8.0 * N * N;
+    int nmag = 0;
+    for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
     qj(p, q);
     if (want_q) cudaMemsetAsync(p->G, 0, sizeof(float2) * LL * nz, p->stream);
     for (int k = 0; k < K; k++) {
       const float2 *psik = psi + (size_t)k * LL;
       const bool need_fwd_chain = (mode != 2) || want_q;
       if (need_fwd_chain) {
+        pbeg(p);
         k_x1<L><<<L / 2, NT, SM, p->stream>>>(psik, p->T1, tb, k, nz, p->magmask);
-        p->launches++;
+        pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * (1 + 4 * nmag + (nz - nmag)));
       }
       for (int j = 0; j < nz; j++) {
         const int mag = (p->magmask >> j) & 1;
@@ -231,32 +293,42 @@ struct Run {
         if (need_fwd_chain) {
           float2 *aout = want_q ? p->Aw : nullptr;
           float2 *w1 = (mode == 2) ? nullptr : p->W1;
+          pbeg(p);
           k_y1<L><<<L / 4, NT, SM, p->stream>>>(T1j, qjj, aout, w1, tb, k, j, nz, mag, N);
-          p->launches++;
+          pend(p, HOLO_PASS_Y1, A + (w1 ? A + rN * A : 0) + (aout ? A : 0),
+               L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0)));
         }
         double *pf = p->partF + fr * nbx2;
+        pbeg(p);
         if (mode == 1) {
           k_x2<L, X2_FWD><<<nbx2, NT, SM, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, j, N);
-          p->launches++;
+          pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
           continue;
         }
         if (mode == 3) {
           k_x2<L, X2_OBJ><<<nbx2, NT, SM, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, j, N);
-          p->launches++;
+          pend(p, HOLO_PASS_X2, rN * A + NN8 / 2, N * fl * 2);
           continue;
         }
-        if (mode == 0)
+        if (mode == 0) {
           k_x2<L, X2_GRAD><<<nbx2, NT, SM, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, j, N);
-        else
+          pend(p, HOLO_PASS_X2, 2 * rN * A + NN8 / 2, N * fl * 4);
+        } else {
           k_x2<L, X2_ADJ><<<nbx2, NT, SM, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, j, N);
-        k_y2<L><<<L / 4, NT, SM, p->stream>>>(p->V1, p->Aw, qjj, want_q ? p->G + (size_t)j * LL : nullptr,
-                                               gpsi ? p->T3 + (size_t)j * LL : nullptr, tb, k, j, nz, mag, N);
-        p->launches += 2;
+          pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
+        }
+        float2 *Gj = want_q ? p->G + (size_t)j * LL : nullptr;
+        float2 *T3j = gpsi ? p->T3 + (size_t)j * LL : nullptr;
+        pbeg(p);
+        k_y2<L><<<L / 4, NT, SM, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, tb, k, j, nz, mag, N);
+        pend(p, HOLO_PASS_Y2, rN * A + (Gj ? 3 * A : 0) + (T3j ? 2 * A : 0),
+             L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0)));
       }
       if (gpsi && (mode == 0 || mode == 2)) {
+        pbeg(p);
         k_x3<L><<<L / 2, NT, SM, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
                                                p->partX3 + (size_t)k * L, tb, k, nz, p->magmask, gscale);
-        p->launches++;
+        pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
       }
     }
     if (want_q && (mode == 0 || mode == 2)) gq(p, gq_out, gscale, false);
@@ -408,6 +480,7 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
 void holo_plan_destroy(holo_plan *p) {
   if (!p) return;
   cudaSetDevice(p->device);
+  for (cudaEvent_t e : p->evpool) cudaEventDestroy(e);
   for (void *a : p->allocs) cudaFree(a);
   delete p;
 }
@@ -417,6 +490,27 @@ size_t holo_plan_workspace_bytes(const holo_plan *p) { return p ? p->ws_bytes : 
 const char *holo_last_error(const holo_plan *p) { return p ? p->err.c_str() : "null plan"; }
 
 uint64_t holo_launch_count(const holo_plan *p) { return p ? p->launches : 0; }
+
+holo_status holo_profile_enable(holo_plan *p, int enable) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  p->prof_on = enable != 0;
+  return HOLO_OK;
+}
+
+holo_status holo_profile_read(holo_plan *p, double *ms, uint64_t *launches, double *bytes, double *flops, int reset) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  prof_flush(p);
+  for (int i = 0; i < HOLO_NPASS; i++) {
+    if (ms) ms[i] = p->pms[i];
+    if (launches) launches[i] = p->pcnt[i];
+    if (bytes) bytes[i] = p->pbytes[i];
+    if (flops) flops[i] = p->pflops[i];
+    if (reset) { p->pms[i] = 0; p->pcnt[i] = 0; p->pbytes[i] = 0; p->pflops[i] = 0; }
+  }
+  return postcheck(p);
+}
 
 holo_status holo_plan_derived(const holo_plan *p, double *m0, double *mt, double *zdet, double *omega, double *zeta,
                               double *p0) {
@@ -498,11 +592,13 @@ holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float 
   dispatch_sweep<Run>(p, obj ? 3 : 0, (const float2 *)psi, (const float2 *)q, sqrt_d, (const float2 *)nullptr,
                       (float2 *)nullptr, (const float2 *)eta_psi_prev, obj ? nullptr : (float2 *)grad_psi,
                       obj ? nullptr : (float2 *)grad_q_part, 2.0f, !obj && grad_q_part != nullptr);
+  pbeg(p);
   k_reduce<<<1, 1024, 0, p->stream>>>(p->partF, (size_t)K * nz * ((N + 3) / 4), 1, sc, 0);
-  p->launches++;
+  pend(p, HOLO_PASS_REDUCE, 8.0 * K * nz * ((N + 3) / 4), 0);
   if (!obj && grad_psi) {
+    pbeg(p);
     k_reduce<<<1, 1024, 0, p->stream>>>(p->partX3, (size_t)K * (L / 2), 2, sc + 1, 0);
-    p->launches++;
+    pend(p, HOLO_PASS_REDUCE, 8.0 * K * L, 0);
   }
   return postcheck(p);
 }
@@ -520,9 +616,12 @@ holo_status holo_q_dots(holo_plan *p, const void *grad_q, const void *eta_q_prev
   if (st != HOLO_OK) return st;
   if (!grad_q || !out) return fail(p, HOLO_EINVAL, "null pointer");
   const size_t n = (size_t)p->L * p->L;
+  pbeg(p);
   k_dots<<<1184, 256, 0, p->stream>>>((const float2 *)grad_q, (const float2 *)eta_q_prev, n, p->partQ);
+  pend(p, HOLO_PASS_REDUCE, 8.0 * n * (eta_q_prev ? 2 : 1), 0);
+  pbeg(p);
   k_reduce<<<1, 1024, 0, p->stream>>>(p->partQ, 1184, 2, out, 0);
-  p->launches += 2;
+  pend(p, HOLO_PASS_REDUCE, 16.0 * 1184, 0);
   return postcheck(p);
 }
 
@@ -555,15 +654,17 @@ holo_status holo_cg_step(holo_plan *p, const holo_cg_in *in, holo_cg_out *out, c
   out->reset = reset;
   const size_t LL = (size_t)p->L * p->L;
   if (psi && eta_psi && psi_trial && (grad_psi || mode == 2)) {
+    pbeg(p);
     k_cg<<<1184, 256, 0, p->stream>>>((const float4 *)psi, (float4 *)eta_psi, (const float4 *)grad_psi,
                                       (float4 *)psi_trial, LL * p->K / 2, (float)in->rho_psi, (float)beta,
                                       (float)in->gamma, mode);
-    p->launches++;
+    pend(p, HOLO_PASS_CG, 8.0 * LL * p->K * (mode == 2 ? 3 : mode == 0 ? 4 : 5), 0);
   }
   if (q && eta_q && q_trial && (grad_q || mode == 2)) {
+    pbeg(p);
     k_cg<<<1184, 256, 0, p->stream>>>((const float4 *)q, (float4 *)eta_q, (const float4 *)grad_q, (float4 *)q_trial,
                                       LL / 2, (float)in->rho_q, (float)beta, (float)in->gamma, mode);
-    p->launches++;
+    pend(p, HOLO_PASS_CG, 8.0 * LL * (mode == 2 ? 3 : mode == 0 ? 4 : 5), 0);
   }
   return postcheck(p);
 }

@@ -1,0 +1,113 @@
+"""Joint psi/q Dai-Yuan CG driver (Eqs. (13)-(14)) over libholo.
+
+Host-side control only: every array operation runs in libholo's kernels
+(holo_grad, holo_q_dots, holo_cg_step); torch provides the buffers and, across
+ranks, torch.distributed (NCCL) for the two exchange steps of a sweep:
+allreduce(sum) of the local probe-gradient partial and of the 3 fp64 psi-block
+scalars.  The q-block dots are then computed redundantly on every rank.
+
+Product-space CG with one shared step (reading C9), block preconditioner
+P = diag(rho_psi, rho_q), Re<.,.> everywhere (C11), halving line search with a
+monotone-F acceptance test (C10).  One host synchronisation per sweep: the
+D2H copy of 5 doubles (F, |g_psi|^2, Re<g_psi, eta_psi>, |g_q|^2, Re<g_q, eta_q>).
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+import torch.distributed as dist
+
+from . import HoloCgIn
+
+
+class JointCG:
+    def __init__(self, plan, sqrt_d, psi0, q0, rho_psi=1.0, rho_q=1.0, gamma_init=1.0, max_halvings=12,
+                 group=None, distributed=None):
+        self.plan = plan
+        self.d = sqrt_d
+        self.rho = (float(rho_psi), float(rho_q))
+        self.gamma_init, self.max_halvings = float(gamma_init), int(max_halvings)
+        self.group = group
+        self.dist = dist.is_available() and dist.is_initialized() if distributed is None else distributed
+        dev = psi0.device
+        z = lambda t: torch.zeros_like(t)
+        self.psi, self.q = psi0.contiguous().clone(), q0.contiguous().clone()
+        self.psi_t, self.q_t = z(self.psi), z(self.q)
+        self.eta_psi, self.eta_q = z(self.psi), z(self.q)
+        self.g_psi, self.g_q = z(self.psi), z(self.q)
+        self.gt_psi, self.gt_q = z(self.psi), z(self.q)
+        self.sc = torch.zeros(5, dtype=torch.float64, device=dev)
+        self.F = None
+        self.dots = None
+        self.g_eta = 0.0          # Re<g_m, eta_{m-1}>
+        self.gprev_eta = 0.0      # Re<g_{m-1}, eta_{m-1}>
+        self.gamma_last = None
+        self.stagnated = True
+        self.m = 0
+        self.sweeps = 0
+
+    # ------------------------------------------------------------------ sweep
+    def sweep(self, psi, q, eta_psi, eta_q, g_psi, g_q):
+        """F and grad at (psi, q); returns host (F, gg_psi, geta_psi, gg_q, geta_q)."""
+        p = self.plan
+        sc3 = self.sc[:3]
+        p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
+        if self.dist:
+            # exchange 1: probe-gradient partial (complex64 viewed as float32), exchange 2: scalars
+            dist.all_reduce(torch.view_as_real(g_q), group=self.group)
+            dist.all_reduce(sc3, group=self.group)
+        p.q_dots(g_q, eta_q, self.sc[3:])
+        s = self.sc.cpu().tolist()  # the single host sync of the sweep
+        self.sweeps += 1
+        if not math.isfinite(s[0]):
+            raise FloatingPointError(f"non-finite objective F = {s[0]} at iteration {self.m}")
+        return s
+
+    def start(self):
+        s = self.sweep(self.psi, self.q, None, None, self.g_psi, self.g_q)
+        self.F = s[0]
+        self.dots = s
+        return self.F
+
+    def gPg(self):
+        return self.rho[0] * self.dots[1] + self.rho[1] * self.dots[3]
+
+    # ------------------------------------------------------------------ one CG iteration
+    def iterate(self, forced_gamma=None):
+        if self.F is None:
+            self.start()
+        p = self.plan
+        first = self.m == 0 or self.stagnated
+        gamma = self.gamma_init if first else self.gamma_last
+        if forced_gamma is not None:
+            gamma = float(forced_gamma)
+        cin = HoloCgIn(self.gPg(), self.g_eta, self.gprev_eta, gamma, self.rho[0], self.rho[1], int(first), 0)
+        out = p.cg_step(cin, self.psi, self.eta_psi, self.g_psi, self.psi_t, self.q, self.eta_q, self.g_q, self.q_t)
+        g_eta_new = out.g_eta_new
+        accepted = False
+        tries = 0
+        while True:
+            s = self.sweep(self.psi_t, self.q_t, self.eta_psi, self.eta_q, self.gt_psi, self.gt_q)
+            tries += 1
+            if forced_gamma is not None or s[0] < self.F:
+                accepted = True
+                break
+            if tries > self.max_halvings:
+                break
+            gamma *= 0.5
+            cin = HoloCgIn(0.0, 0.0, 0.0, gamma, self.rho[0], self.rho[1], 0, 1)
+            p.cg_step(cin, self.psi, self.eta_psi, None, self.psi_t, self.q, self.eta_q, None, self.q_t)
+        if accepted:
+            self.psi, self.psi_t = self.psi_t, self.psi
+            self.q, self.q_t = self.q_t, self.q
+            self.g_psi, self.gt_psi = self.gt_psi, self.g_psi
+            self.g_q, self.gt_q = self.gt_q, self.g_q
+            self.F, self.dots = s[0], s
+            self.gprev_eta = g_eta_new
+            self.g_eta = s[2] + s[4]
+            self.gamma_last, self.stagnated = gamma, False
+        else:
+            gamma, self.stagnated = 0.0, True
+        self.m += 1
+        return dict(F=self.F, gamma=gamma, beta=out.beta, reset=bool(out.reset), sweeps=tries)
