@@ -1,20 +1,32 @@
-// fft_engine.cuh -- shared-memory Stockham line FFT for sm_100a.
+// fft_engine.cuh -- register-resident Stockham line FFT for sm_100a.
 //
-// One "group" of TPL = L/16 threads transforms one length-L complex64 line that
-// lives in shared memory.  A CTA runs G groups side by side on G line buffers
-// (all groups pass the same __syncthreads(), so every thread of the CTA must call
-// the transform even when its group has no line: active = false).
+// A length-L complex64 line (L = F * 16^S16, F in {2, 4, 8, 16}) is held by a
+// "group" of T = L/16 threads, 16 values per thread, in LAYOUT S:
 //
-// Factorisation: L = F * 16^s with a first radix F in {2, 4, 8, 16} (Ns = 1, no
-// twiddles) followed by s radix-16 Stockham stages (self-sorting, natural order
-// in and out).  Each radix-16 butterfly is done in registers (radix-2 DIF with
-// compile-time twiddles); stage twiddles exp(-2 pi i m r / (16 Ns)) come from an
-// fp64-generated table laid out [stage][r-1][m] so consecutive threads read
-// consecutive entries.
+//     thread t, register r  <->  element t + T*r            (r = 0..15)
 //
-// Shared-memory layout: element i of a line sits at P(i) = i + (i >> 4) (one pad
-// slot every 16 complex) which makes both the strided reads and the radix-16 /
-// radix-F Stockham scatters bank-conflict free for 64-bit accesses.
+// Stockham autosort (natural order in and out).  Stage 0 is radix F (Ns = 1,
+// no twiddles; thread t runs the 16/F butterflies j = t + T*b); then S16
+// radix-16 stages with Ns = F, 16F, ..., L/16.  Every stage reads its inputs in
+// layout S, and the LAST stage (Ns = T, so m = t) also WRITES layout S: the
+// result stays in the same registers and pointwise factors (chirps, transfer
+// functions, probe) are applied there, between transforms, with no shared-memory
+// round trip.  Only the S16 exchanges between stages go through shared memory:
+// 2 per transform for L = 512 ... 4096 (one STS.64 + one LDS.64 per element each).
+//
+// Exchange buffers are double-buffered per group: exchange e writes buffer e&1,
+// which makes ONE __syncthreads() per exchange sufficient (the next write to the
+// same buffer is two exchanges later, behind another barrier that every reader
+// of this one has passed).  Element i sits at padded slot P(i) = i + i/16, so the
+// layout-S reads and the radix-16 / radix-F scatters are bank-conflict free for
+// 64-bit accesses within a group.
+//
+// Stage twiddles w^{m s}, w = exp(-2 pi i / (16 Ns)), s = 1..15: the table holds
+// only w^m, w^2m, w^4m, w^8m per m (fp64-generated, one 32-byte row); the other
+// eleven are products of at most three of them (<= 3 roundings in fp32).
+//
+// Every thread of the CTA must call every transform (barriers); lines without
+// data simply transform zeros.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -22,14 +34,6 @@
 namespace holo {
 
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }
-
-// Read-only table load that the compiler may not hoist or CSE across transforms
-// (keeping a whole stage of twiddles live across FFT calls costs ~60 registers).
-__device__ __forceinline__ float2 ldtw(const float2 *p) {
-  float2 v;
-  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-  return v;
-}
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
@@ -42,12 +46,12 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+__device__ __forceinline__ float2 ldg2(const float2 *p) { return __ldg(p); }
 
 // Multiply by W16^e = exp(-+2 pi i e / 16) (forward: minus), e in [0, 8), compile-time.
 template <int E, bool INV>
 __device__ __forceinline__ float2 tw16(float2 x) {
   constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f, H = 0.70710678118654752f;
-  // forward: x * (c - i s);  inverse: x * (c + i s)
   if constexpr (E == 0) {
     return x;
   } else if constexpr (E == 4) {
@@ -66,8 +70,9 @@ __device__ __forceinline__ float2 tw16(float2 x) {
 
 __host__ __device__ constexpr int ilog2c(int n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
 __host__ __device__ constexpr int brevc(int i, int bits) { return bits == 0 ? 0 : ((i & 1) << (bits - 1)) | brevc(i >> 1, bits - 1); }
+__host__ __device__ constexpr int pow16(int e) { return e == 0 ? 1 : 16 * pow16(e - 1); }
 
-// radix-2 DIF level with half-span H on R registers
+// radix-2 DIF level with half-span H on R registers starting at v[O], stride D
 template <int R, int H, bool INV>
 struct DifLevel {
   template <int I>
@@ -89,7 +94,6 @@ struct DifLevel {
   }
 };
 
-// compile-time bit-reversal permutation of R registers (pure renaming after inlining)
 template <int R, int I>
 struct BrevPerm {
   __device__ __forceinline__ static void run(const float2 *v, float2 *t) {
@@ -112,75 +116,97 @@ __device__ __forceinline__ void dft_reg(float2 *v) {
 }
 
 template <int L>
-struct FftShape {
-  static constexpr int S16 = (ilog2c(L) - 1) / 4;  // radix-16 stages
-  static constexpr int F = L >> (4 * S16);          // first radix (2, 4, 8 or 16)
-  static constexpr int TPL = L / 16;                                                // threads per line
+struct Shape {
+  static constexpr int LOG = ilog2c(L);
+  static constexpr int S16 = (LOG - 1) / 4;  // radix-16 stages after the first
+  static constexpr int F = L >> (4 * S16);   // first radix
+  static constexpr int T = L / 16;           // threads per line
+  static constexpr int PER = 16 / F;         // stage-0 butterflies per thread
+  static constexpr int LP = L + L / 16;      // padded line (float2)
+  // twiddle rows (4 float2 = 2 float4 each): sum over radix-16 stages of Ns
+  static constexpr int TWROWS = F * (pow16(S16) - 1) / 15;
   static_assert(F == 2 || F == 4 || F == 8 || F == 16, "unsupported L");
-  static_assert((1 << ilog2c(L)) == L, "L must be a power of two");
-  static constexpr int TW = L - F;  // twiddle table entries (radix-16 stages)
+  static_assert((1 << LOG) == L && L >= 128, "L must be a power of two >= 128");
 };
 
-// Stage twiddle table: after the first radix-F stage (Ns = 1, no twiddles) the
-// radix-16 stages have Ns = F, 16F, 256F, ...; stage Ns uses 15*Ns entries
-// [(r-1)*Ns + m] = exp(-2 pi i m r / (16 Ns)) at offset sum_{previous} 15*Ns.
+// Exchange space of one line: two buffers of LP float2 at b and b + LPB.
+struct Xch {
+  float2 *b;
+  int par;
+  int stride;
+  __device__ __forceinline__ float2 *next() {
+    float2 *p = par ? b + stride : b;
+    par ^= 1;
+    return p;
+  }
+};
 
-// Transform a padded smem line in place.  t = thread index in the group [0, TPL).
-template <int L, bool INV>
-__device__ __noinline__ void fft_line(float2 *buf, const float2 *__restrict__ tw, int t, bool active) {
-  using S = FftShape<L>;
-  constexpr int TPL = S::TPL;
-  constexpr int F = S::F;
-  // ---- first stage: radix F, Ns = 1, 16/F butterflies per thread
+template <bool INV>
+__device__ __forceinline__ void twmul(float2 &v, float2 w) { v = INV ? cmulc(v, w) : cmul(v, w); }
+
+template <int L, bool INV, int ST>
+__device__ __forceinline__ void r16_stage(float2 (&v)[16], Xch &x, const int t, const float4 *__restrict__ tw) {
+  using S = Shape<L>;
+  constexpr int Ns = S::F * pow16(ST);
+  constexpr int ROW0 = S::F * (pow16(ST) - 1) / 15;
+  const int m = t & (Ns - 1);
   {
-    constexpr int NB = L / F;
-    constexpr int PER = 16 / F;
-    float2 v[PER][F];
-    if (active) {
-#pragma unroll
-      for (int b = 0; b < PER; b++)
-#pragma unroll
-        for (int r = 0; r < F; r++) v[b][r] = buf[P(t + b * TPL + r * NB)];
-    }
-    __syncthreads();
-    if (active) {
-#pragma unroll
-      for (int b = 0; b < PER; b++) {
-        dft_reg<F, INV>(v[b]);
-        const int j = t + b * TPL;
-#pragma unroll
-        for (int r = 0; r < F; r++) buf[P(j * F + r)] = v[b][r];
-      }
-    }
-    __syncthreads();
+    const float4 a = __ldg(tw + 2 * (ROW0 + m)), b = __ldg(tw + 2 * (ROW0 + m) + 1);
+    const float2 w1 = make_float2(a.x, a.y), w2 = make_float2(a.z, a.w), w4 = make_float2(b.x, b.y),
+                 w8 = make_float2(b.z, b.w);
+    twmul<INV>(v[1], w1);
+    twmul<INV>(v[2], w2);
+    twmul<INV>(v[4], w4);
+    twmul<INV>(v[8], w8);
+    const float2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+    twmul<INV>(v[3], w3);
+    twmul<INV>(v[5], w5);
+    twmul<INV>(v[6], w6);
+    twmul<INV>(v[7], w7);
+    twmul<INV>(v[9], cmul(w1, w8));
+    twmul<INV>(v[10], cmul(w2, w8));
+    twmul<INV>(v[11], cmul(w3, w8));
+    twmul<INV>(v[12], cmul(w4, w8));
+    twmul<INV>(v[13], cmul(w5, w8));
+    twmul<INV>(v[14], cmul(w6, w8));
+    twmul<INV>(v[15], cmul(w7, w8));
   }
-  // ---- radix-16 stages
-  int off = 0;
+  dft_reg<16, INV>(v);
+  if constexpr (ST + 1 < S::S16) {
+    float2 *buf = x.next();
+    const int base = (t - m) * 16 + m;
 #pragma unroll
-  for (int st = 0, Ns = F; st < S::S16; st++, Ns *= 16) {
-    constexpr int NB = L / 16;  // == TPL
-    float2 v[16];
-    if (active) {
-#pragma unroll
-      for (int r = 0; r < 16; r++) v[r] = buf[P(t + r * NB)];
-    }
+    for (int s = 0; s < 16; s++) buf[P(base + s * Ns)] = v[s];
     __syncthreads();
-    if (active) {
-      const int m = t & (Ns - 1);
-      const float2 *tws = tw + off + m;
 #pragma unroll
-      for (int r = 1; r < 16; r++) {
-        float2 w = ldtw(tws + (r - 1) * Ns);
-        v[r] = INV ? cmulc(v[r], w) : cmul(v[r], w);
-      }
-      dft_reg<16, INV>(v);
-      const int base = (t - m) * 16 + m;
-#pragma unroll
-      for (int r = 0; r < 16; r++) buf[P(base + r * Ns)] = v[r];
-    }
-    __syncthreads();
-    off += 15 * Ns;
+    for (int r = 0; r < 16; r++) v[r] = buf[P(t + r * S::T)];
+    r16_stage<L, INV, ST + 1>(v, x, t, tw);
   }
+}
+
+// In-place transform of the line held in layout S (unnormalised; INV: exp(+...)).
+template <int L, bool INV>
+__device__ __forceinline__ void fft(float2 (&v)[16], Xch &x, const int t, const float4 *__restrict__ tw) {
+  using S = Shape<L>;
+  constexpr int F = S::F, PER = S::PER;
+#pragma unroll
+  for (int b = 0; b < PER; b++) {
+    float2 u[F];
+#pragma unroll
+    for (int s = 0; s < F; s++) u[s] = v[b + PER * s];
+    dft_reg<F, INV>(u);
+#pragma unroll
+    for (int s = 0; s < F; s++) v[b + PER * s] = u[s];
+  }
+  float2 *buf = x.next();
+#pragma unroll
+  for (int b = 0; b < PER; b++)
+#pragma unroll
+    for (int s = 0; s < F; s++) buf[P((t + S::T * b) * F + s)] = v[b + PER * s];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = buf[P(t + r * S::T)];
+  r16_stage<L, INV, 0>(v, x, t, tw);
 }
 
 }  // namespace holo

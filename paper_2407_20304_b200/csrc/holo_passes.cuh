@@ -1,5 +1,9 @@
 // holo_passes.cuh -- the five line-pass kernels (X1, Y1, X2, Y2, X3), the
 // propagation filters for q_j / g_q, reductions and the CG pointwise step.
+//
+// All line kernels: 512 threads, G = 512 / (L/16) lines per CTA, one CTA per SM
+// at L = 4096 (<= 128 registers; exchange buffers + one thread-private line in
+// shared memory).
 #pragma once
 #include "holo_kernels.cuh"
 
@@ -7,279 +11,251 @@ namespace holo {
 
 enum { X2_GRAD = 0, X2_FWD = 1, X2_ADJ = 2, X2_OBJ = 3 };
 
+template <int L, bool COLS>
+__device__ __forceinline__ float2 *priv_base(float2 *sm) {
+  return sm + Cta<L, COLS>::XBYTES / sizeof(float2);
+}
+
 // ----------------------------------------------------------------------------- X1
-// rows of psi_k (2 rows / CTA):  X = FFT(psi row); per j: T1_j row = M_{1/mt_j} S_{sx} psi row
+// rows of psi_k:  X = FFT(psi row) (kept thread-private); per j: T1_j row = M_{1/mt_j} S_{sx} psi row
 template <int L>
-__global__ void __launch_bounds__(Cfg<L>::NT, 1) k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1,
-                                                    Tables tb, int k, int nz, uint32_t magmask) {
-  using C = Cfg<L>;
-  extern __shared__ float2 sm[];
-  float2 *X0 = sm, *X1 = sm + C::LPB, *A0 = sm + 2 * C::LPB, *B0 = sm + 3 * C::LPB, *A1 = sm + 4 * C::LPB,
-         *B1 = sm + 5 * C::LPB;
-  float2 *Xs[2] = {X0, X1}, *As[2] = {A0, A1}, *Bs[2] = {B0, B1};
-  const int y0 = blockIdx.x * 2;
-  load_rows<L>(Xs, psi_k, L, y0, 2, 2);
-  __syncthreads();
-  fft4<L, false>(X0, nullptr, X1, nullptr, tb.tw);
+__global__ void __launch_bounds__(512, 1)
+    k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1, Tables tb, int k, int nz, uint32_t magmask) {
+  using C = Cta<L, false>;
+  extern __shared__ float4 sm4[];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const Priv<512> X{priv_base<L, false>(sm)};
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  float2 v[16];
+  ld_row<L>(v, psi_k + (size_t)y * L, t);
+  fft<L, false>(v, x, t, tb.tw);
+#pragma unroll
+  for (int r = 0; r < 16; r++) X[r] = v[r];
   for (int j = 0; j < nz; j++) {
-    const float2 *rx = tb.ramps + ((size_t)(k * nz + j) * 2 + 0) * L;
-    const float2 *rr[2] = {rx, rx};
+    const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 0) * L;
     if ((magmask >> j) & 1u) {
-      bl_pre_fwd<L>(Xs, As, Bs, 2, tb.cin + j * L, rr, tb.wodd);
-      __syncthreads();
-      fft4<L, false>(A0, B0, A1, B1, tb.tw);
-      bl_mul<L, false>(As, Bs, 2, tb.bke + j * L, tb.bko + j * L);
-      __syncthreads();
-      fft4<L, true>(A0, B0, A1, B1, tb.tw);
-      bl_post_fwd<L>(As, Bs, 2, tb.cout + j * L, tb.wodd);
+      mag_fwd<L>(v, [&](int r) { return X[r]; }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
     } else {
-      for (int e = threadIdx.x; e < 2 * L; e += blockDim.x) {
-        int l = e / L, i = e % L;
-        As[l][P(i)] = cscale(cmul(Xs[l][P(i)], __ldg(rx + i)), 1.0f / L);
-      }
-      __syncthreads();
-      fft4<L, true>(A0, nullptr, A1, nullptr, tb.tw);
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cmul(X[r], ldg2(cr + t + r * (L / 16)));
+      fft<L, true>(v, x, t, tb.tw);
     }
-    __syncthreads();
-    store_rows<L>(As, T1 + (size_t)j * L * L, L, y0, 2, 2, 1.0f);
-    __syncthreads();
+    st_row<L>(v, T1 + (size_t)j * L * L + (size_t)y * L, t);
   }
 }
 
 // ----------------------------------------------------------------------------- Y1
-// 4 columns / CTA of T1_j:  a = M_{1/mt_j} S_{sy} (column);  optionally store a;
+// columns of T1_j:  a = M_{1/mt_j} S_{sy} (column);  optionally store a;
 // optionally  W1 = rows [o, o+N) of D_y(q_j . a)
 template <int L>
-__global__ void __launch_bounds__(Cfg<L>::NT, 1)
+__global__ void __launch_bounds__(512, 1)
     k_y1(const float2 *__restrict__ T1j, const float2 *__restrict__ qj, float2 *__restrict__ Aout,
          float2 *__restrict__ W1, Tables tb, int k, int j, int nz, int mag, int N) {
-  using C = Cfg<L>;
-  extern __shared__ float2 sm[];
-  float2 *Cl[4] = {sm, sm + C::LPB, sm + 2 * C::LPB, sm + 3 * C::LPB};
-  float2 *S0 = sm + 4 * C::LPB, *S1 = sm + 5 * C::LPB;
-  const int x0 = blockIdx.x * 4;
-  load_cols4<L>(Cl, T1j, x0, 0, L, 0);
-  __syncthreads();
-  fft4<L, false>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-  const float2 *ry = tb.ramps + ((size_t)(k * nz + j) * 2 + 1) * L;
+  using C = Cta<L, true>;
+  constexpr int T = L / 16;
+  extern __shared__ float4 sm4[];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const Priv<512> X{priv_base<L, true>(sm)};
+  const int t = C::t(), col = blockIdx.x * C::G + C::g();
+  const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 1) * L;
+  float2 v[16];
+  ld_col<L>(v, T1j + col, t);
+  fft<L, false>(v, x, t, tb.tw);
   if (mag) {
-    const float2 *rr[2] = {ry, ry};
-    for (int rd = 0; rd < 2; rd++) {
-      float2 *Ap[2] = {Cl[2 * rd], Cl[2 * rd + 1]}, *Bp[2] = {S0, S1};
-      bl_pre_fwd<L>(Ap, Ap, Bp, 2, tb.cin + j * L, rr, tb.wodd);
-      __syncthreads();
-      fft4<L, false>(Ap[0], S0, Ap[1], S1, tb.tw);
-      bl_mul<L, false>(Ap, Bp, 2, tb.bke + j * L, tb.bko + j * L);
-      __syncthreads();
-      fft4<L, true>(Ap[0], S0, Ap[1], S1, tb.tw);
-      bl_post_fwd<L>(Ap, Bp, 2, tb.cout + j * L, tb.wodd);
-      __syncthreads();
-    }
+#pragma unroll
+    for (int r = 0; r < 16; r++) X[r] = v[r];
+    mag_fwd<L>(v, [&](int r) { return X[r]; }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
   } else {
-    mul_lines<L, false>(Cl, 4, ry, 1.0f / L);
-    __syncthreads();
-    fft4<L, true>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
+    mul_tab<L, false>(v, cr, t);
+    fft<L, true>(v, x, t, tb.tw);
   }
-  if (Aout) store_cols4<L>(Cl, Aout, x0, 0, L, 0, 1.0f);
+  if (Aout) st_col<L>(v, Aout + col, t);
   if (W1) {
-    for (int e = threadIdx.x; e < 2 * L; e += blockDim.x) {
-      int y = e >> 1, h = e & 1;
-      float4 q = __ldg(reinterpret_cast<const float4 *>(qj + (size_t)y * L + x0 + 2 * h));
-      Cl[2 * h][P(y)] = cmul(Cl[2 * h][P(y)], make_float2(q.x, q.y));
-      Cl[2 * h + 1][P(y)] = cmul(Cl[2 * h + 1][P(y)], make_float2(q.z, q.w));
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + (size_t)(t + r * T) * L + col));
+    fft<L, false>(v, x, t, tb.tw);
+    mul_tab<L, false>(v, tb.hdet + (size_t)j * L, t);
+    fft<L, true>(v, x, t, tb.tw);
+    const int o = (L - N) / 2;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int row = t + r * T - o;
+      if (row >= 0 && row < N) W1[(size_t)row * L + col] = v[r];
     }
-    __syncthreads();
-    fft4<L, false>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-    mul_lines<L, false>(Cl, 4, tb.hdet + j * L, 1.0f / L);
-    __syncthreads();
-    fft4<L, true>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-    store_cols4<L>(Cl, W1, x0, 0, N, (L - N) / 2, 1.0f);
   }
 }
 
 // ----------------------------------------------------------------------------- X2
-// 4 rows / CTA.  GRAD: W1 row -> D_x, crop, residual (+F), pad, D_x^* -> V1
-//                FWD : W1 row -> D_x, crop -> w frame [N][N]
-//                ADJ : y frame row -> pad, D_x^* -> V1
-//                OBJ : W1 row -> D_x, crop, F only
+// rows y < N.  GRAD: W1 row -> D_x, crop, residual (+F), pad, D_x^* -> V1
+//              FWD : W1 row -> D_x, crop -> w frame [N][N]
+//              ADJ : y frame row -> pad, D_x^* -> V1
+//              OBJ : W1 row -> D_x, crop, F only
 template <int L, int MODE>
-__global__ void __launch_bounds__(Cfg<L>::NT, 1)
+__global__ void __launch_bounds__(512, 1)
     k_x2(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
          double *__restrict__ partial, Tables tb, int j, int N) {
-  using C = Cfg<L>;
-  extern __shared__ float2 sm[];
+  using C = Cta<L, false>;
+  constexpr int T = L / 16;
+  extern __shared__ float4 sm4[];
   __shared__ double red[32];
-  float2 *Cl[4] = {sm, sm + C::LPB, sm + 2 * C::LPB, sm + 3 * C::LPB};
-  const int y0 = blockIdx.x * 4;
-  const int nvalid = min(4, N - y0);
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  const bool act = y < N;
   const int o = (L - N) / 2;
+  const float2 *h = tb.hdet + (size_t)j * L;
+  float2 v[16];
   if (MODE != X2_ADJ) {
-    load_rows<L>(Cl, in, L, y0, 4, nvalid);
-    __syncthreads();
-    fft4<L, false>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-    mul_lines<L, false>(Cl, 4, tb.hdet + j * L, 1.0f / L);
-    __syncthreads();
-    fft4<L, true>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = act ? ldg2(in + (size_t)y * L + t + r * T) : make_float2(0.f, 0.f);
+    fft<L, false>(v, x, t, tb.tw);
+    mul_tab<L, false>(v, h, t);
+    fft<L, true>(v, x, t, tb.tw);
     if (MODE == X2_FWD) {
-      for (int e = threadIdx.x; e < 4 * N; e += blockDim.x) {
-        int l = e / N, x = e % N;
-        if (l < nvalid) out[(size_t)(y0 + l) * N + x] = Cl[l][P(o + x)];
+      if (act) {
+#pragma unroll
+        for (int r = 0; r < 16; r++) {
+          const int c = t + r * T - o;
+          if (c >= 0 && c < N) out[(size_t)y * N + c] = v[r];
+        }
       }
       return;
     }
     double acc = 0.0;
-    for (int e = threadIdx.x; e < 4 * L; e += blockDim.x) {
-      int l = e / L, x = e % L;
-      float2 v = make_float2(0.f, 0.f);
-      if (l < nvalid && x >= o && x < o + N) {
-        float2 w = Cl[l][P(x)];
-        float d = __ldg(sqrt_d + (size_t)(y0 + l) * N + (x - o));
-        float m = sqrtf(w.x * w.x + w.y * w.y);
-        float dm = m - d;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int c = t + r * T - o;
+      float2 w = make_float2(0.f, 0.f);
+      if (act && c >= 0 && c < N) {
+        const float d = __ldg(sqrt_d + (size_t)y * N + c);
+        const float m = sqrtf(v[r].x * v[r].x + v[r].y * v[r].y);
+        const float dm = m - d;
         acc += (double)(dm * dm);
-        float f = m > 0.f ? 1.0f - d / m : 0.f;  // rho = w - d w/|w|, 0 at w = 0 (C7)
-        v = cscale(w, f);
+        const float f = m > 0.f ? 1.0f - d / m : 0.f;  // rho = w - d w/|w|, 0 at w = 0 (C7)
+        w = cscale(v[r], f);
       }
-      Cl[l][P(x)] = v;
+      v[r] = w;
     }
-    double s = block_sum(acc, red);
+    const double s = block_sum(acc, red);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
     if (MODE == X2_OBJ) return;
   } else {
-    for (int e = threadIdx.x; e < 4 * L; e += blockDim.x) {
-      int l = e / L, x = e % L;
-      float2 v = make_float2(0.f, 0.f);
-      if (l < nvalid && x >= o && x < o + N) v = in[(size_t)(y0 + l) * N + (x - o)];
-      Cl[l][P(x)] = v;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int c = t + r * T - o;
+      v[r] = (act && c >= 0 && c < N) ? ldg2(in + (size_t)y * N + c) : make_float2(0.f, 0.f);
     }
   }
-  __syncthreads();
-  fft4<L, false>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-  mul_lines<L, true>(Cl, 4, tb.hdet + j * L, 1.0f / L);
-  __syncthreads();
-  fft4<L, true>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-  store_rows<L>(Cl, out, L, y0, 4, nvalid, 1.0f);
+  fft<L, false>(v, x, t, tb.tw);
+  mul_tab<L, true>(v, h, t);
+  fft<L, true>(v, x, t, tb.tw);
+  if (act) st_row<L>(v, out + (size_t)y * L, t);
 }
 
 // ----------------------------------------------------------------------------- Y2
-// 4 columns / CTA:  v = D_y^* pad(V1 col);  G_j += conj(a) v;  T3_j = (M S)_y^*(conj(q_j) v)
+// columns:  v = D_y^* pad(V1 col);  G_j += conj(a) v;  T3_j = (M S)_y^*(conj(q_j) v)
 template <int L>
-__global__ void __launch_bounds__(Cfg<L>::NT, 1)
+__global__ void __launch_bounds__(512, 1)
     k_y2(const float2 *__restrict__ V1, const float2 *__restrict__ a, const float2 *__restrict__ qj,
          float2 *__restrict__ Gj, float2 *__restrict__ T3j, Tables tb, int k, int j, int nz, int mag, int N) {
-  using C = Cfg<L>;
-  extern __shared__ float2 sm[];
-  float2 *Cl[4] = {sm, sm + C::LPB, sm + 2 * C::LPB, sm + 3 * C::LPB};
-  float2 *S0 = sm + 4 * C::LPB, *S1 = sm + 5 * C::LPB;
-  const int x0 = blockIdx.x * 4;
+  using C = Cta<L, true>;
+  constexpr int T = L / 16;
+  extern __shared__ float4 sm4[];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const Priv<512> Y{priv_base<L, true>(sm)};
+  const int t = C::t(), col = blockIdx.x * C::G + C::g();
   const int o = (L - N) / 2;
-  for (int e = threadIdx.x; e < 4 * (L - N); e += blockDim.x) {
-    int l = e / (L - N), y = e % (L - N);
-    Cl[l][P(y < o ? y : y + N)] = make_float2(0.f, 0.f);
+  float2 v[16];
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const int row = t + r * T - o;
+    v[r] = (row >= 0 && row < N) ? ldg2(V1 + (size_t)row * L + col) : make_float2(0.f, 0.f);
   }
-  load_cols4<L>(Cl, V1, x0, 0, N, o);
-  __syncthreads();
-  fft4<L, false>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-  mul_lines<L, true>(Cl, 4, tb.hdet + j * L, 1.0f / L);
-  __syncthreads();
-  fft4<L, true>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-  for (int e = threadIdx.x; e < 2 * L; e += blockDim.x) {
-    int y = e >> 1, h = e & 1;
-    size_t gi = (size_t)y * L + x0 + 2 * h;
-    float2 v0 = Cl[2 * h][P(y)], v1 = Cl[2 * h + 1][P(y)];
-    if (Gj) {
-      float4 av = __ldg(reinterpret_cast<const float4 *>(a + gi));
-      float4 g = *reinterpret_cast<float4 *>(Gj + gi);
-      float2 g0 = cadd(make_float2(g.x, g.y), cmulc(v0, make_float2(av.x, av.y)));
-      float2 g1 = cadd(make_float2(g.z, g.w), cmulc(v1, make_float2(av.z, av.w)));
-      *reinterpret_cast<float4 *>(Gj + gi) = make_float4(g0.x, g0.y, g1.x, g1.y);
-    }
-    if (T3j) {
-      float4 q = __ldg(reinterpret_cast<const float4 *>(qj + gi));
-      Cl[2 * h][P(y)] = cmulc(v0, make_float2(q.x, q.y));
-      Cl[2 * h + 1][P(y)] = cmulc(v1, make_float2(q.z, q.w));
+  fft<L, false>(v, x, t, tb.tw);
+  mul_tab<L, true>(v, tb.hdet + (size_t)j * L, t);
+  fft<L, true>(v, x, t, tb.tw);
+  if (Gj) {
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const size_t gi = (size_t)(t + r * T) * L + col;
+      Gj[gi] = cadd(Gj[gi], cmulc(v[r], ldg2(a + gi)));
     }
   }
   if (!T3j) return;
-  __syncthreads();
-  const float2 *ry = tb.ramps + ((size_t)(k * nz + j) * 2 + 1) * L;
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + (size_t)(t + r * T) * L + col));
+  const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 1) * L;
   if (mag) {
-    const float2 *rr[2] = {ry, ry};
-    for (int rd = 0; rd < 2; rd++) {
-      float2 *Ap[2] = {Cl[2 * rd], Cl[2 * rd + 1]}, *Bp[2] = {S0, S1};
-      bl_pre_adj<L>(Ap, Bp, 2, tb.cout + j * L, tb.wodd);
-      __syncthreads();
-      fft4<L, false>(Ap[0], S0, Ap[1], S1, tb.tw);
-      bl_mul<L, true>(Ap, Bp, 2, tb.bke + j * L, tb.bko + j * L);
-      __syncthreads();
-      fft4<L, true>(Ap[0], S0, Ap[1], S1, tb.tw);
-      bl_post_adj<L, false>(Ap, Bp, Ap, 2, tb.cin + j * L, rr, tb.wodd);
-      __syncthreads();
-    }
+#pragma unroll
+    for (int r = 0; r < 16; r++) Y[r] = v[r];
+    mag_adj<L>(v, [&](int r) { return Y[r]; }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
   } else {
-    fft4<L, false>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-    mul_lines<L, true>(Cl, 4, ry, 1.0f / L);
-    __syncthreads();
+    fft<L, false>(v, x, t, tb.tw);
+    mul_tab<L, true>(v, cr, t);
   }
-  fft4<L, true>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-  store_cols4<L>(Cl, T3j, x0, 0, L, 0, 1.0f);
+  fft<L, true>(v, x, t, tb.tw);
+  st_col<L>(v, T3j + col, t);
 }
 
 // ----------------------------------------------------------------------------- X3
-// 2 rows / CTA: g_k row = scale * IFFT( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3_j row;
+// rows: g_k row = scale * IFFT( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3_j row;
 // partial[blk][0] = sum |g|^2, partial[blk][1] = sum Re(g conj(eta))
 template <int L>
-__global__ void __launch_bounds__(Cfg<L>::NT, 1)
+__global__ void __launch_bounds__(512, 1)
     k_x3(const float2 *__restrict__ T3, const float2 *__restrict__ eta, float2 *__restrict__ g,
          double *__restrict__ partial, Tables tb, int k, int nz, uint32_t magmask, float scale) {
-  using C = Cfg<L>;
-  extern __shared__ float2 sm[];
+  using C = Cta<L, false>;
+  constexpr int T = L / 16;
+  extern __shared__ float4 sm4[];
   __shared__ double red[32];
-  float2 *Q0 = sm, *Q1 = sm + C::LPB, *A0 = sm + 2 * C::LPB, *B0 = sm + 3 * C::LPB, *A1 = sm + 4 * C::LPB,
-         *B1 = sm + 5 * C::LPB;
-  float2 *Qs[2] = {Q0, Q1}, *As[2] = {A0, A1}, *Bs[2] = {B0, B1};
-  const int y0 = blockIdx.x * 2;
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const Priv<512> W{priv_base<L, false>(sm)};
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  float2 v[16];
   for (int j = 0; j < nz; j++) {
-    load_rows<L>(As, T3 + (size_t)j * L * L, L, y0, 2, 2);
-    __syncthreads();
-    const float2 *rx = tb.ramps + ((size_t)(k * nz + j) * 2 + 0) * L;
-    const float2 *rr[2] = {rx, rx};
+    const float2 *row = T3 + (size_t)j * L * L + (size_t)y * L;
+    const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 0) * L;
     if ((magmask >> j) & 1u) {
-      bl_pre_adj<L>(As, Bs, 2, tb.cout + j * L, tb.wodd);
-      __syncthreads();
-      fft4<L, false>(A0, B0, A1, B1, tb.tw);
-      bl_mul<L, true>(As, Bs, 2, tb.bke + j * L, tb.bko + j * L);
-      __syncthreads();
-      fft4<L, true>(A0, B0, A1, B1, tb.tw);
-      if (j == 0)
-        bl_post_adj<L, false>(As, Bs, Qs, 2, tb.cin + j * L, rr, tb.wodd);
-      else
-        bl_post_adj<L, true>(As, Bs, Qs, 2, tb.cin + j * L, rr, tb.wodd);
+      mag_adj<L>(v, [&](int r) { return ldg2(row + t + r * T); }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
     } else {
-      fft4<L, false>(A0, nullptr, A1, nullptr, tb.tw);
-      for (int e = threadIdx.x; e < 2 * L; e += blockDim.x) {
-        int l = e / L, i = e % L;
-        float2 w = cscale(cmulc(As[l][P(i)], __ldg(rx + i)), 1.0f / L);
-        Qs[l][P(i)] = j == 0 ? w : cadd(Qs[l][P(i)], w);
-      }
+      ld_row<L>(v, row, t);
+      fft<L, false>(v, x, t, tb.tw);
+      mul_tab<L, true>(v, cr, t);
     }
-    __syncthreads();
+    if (j == 0) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) W[r] = v[r];
+    } else if (j + 1 < nz) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) W[r] = cadd(W[r], v[r]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cadd(W[r], v[r]);
+    }
   }
-  fft4<L, true>(Q0, nullptr, Q1, nullptr, tb.tw);
+  if (nz == 1) {
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = W[r];
+  }
+  fft<L, true>(v, x, t, tb.tw);
   double gg = 0.0, ge = 0.0;
-  for (int e = threadIdx.x; e < L; e += blockDim.x) {  // pairs of elements
-    int l = (2 * e) / L, i = (2 * e) % L;
-    float2 a = cscale(Qs[l][P(i)], scale), b = cscale(Qs[l][P(i + 1)], scale);
-    size_t gi = (size_t)(y0 + l) * L + i;
-    *reinterpret_cast<float4 *>(g + gi) = make_float4(a.x, a.y, b.x, b.y);
-    gg += (double)(a.x * a.x + a.y * a.y) + (double)(b.x * b.x + b.y * b.y);
+  float2 *grow = g + (size_t)y * L;
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const float2 a = cscale(v[r], scale);
+    grow[t + r * T] = a;
+    gg += (double)(a.x * a.x + a.y * a.y);
     if (eta) {
-      float4 ev = __ldg(reinterpret_cast<const float4 *>(eta + gi));
-      ge += (double)(a.x * ev.x + a.y * ev.y) + (double)(b.x * ev.z + b.y * ev.w);
+      const float2 e = ldg2(eta + (size_t)y * L + t + r * T);
+      ge += (double)(a.x * e.x + a.y * e.y);
     }
   }
-  double s0 = block_sum(gg, red);
-  double s1 = block_sum(ge, red);
+  const double s0 = block_sum(gg, red);
+  const double s1 = block_sum(ge, red);
   if (threadIdx.x == 0) {
     partial[2 * blockIdx.x] = s0;
     partial[2 * blockIdx.x + 1] = s1;
@@ -287,55 +263,56 @@ __global__ void __launch_bounds__(Cfg<L>::NT, 1)
 }
 
 // ------------------------------------------------------------------ filters
-// rows (4 / CTA): out = scale * IFFT(h^(*) FFT(in)) along x
+// rows: out = scale * IFFT(h^(*) FFT(in)) / L along x
 template <int L>
-__global__ void __launch_bounds__(Cfg<L>::NT, 1)
+__global__ void __launch_bounds__(512, 1)
     k_rows_filter(const float2 *__restrict__ in, float2 *__restrict__ out, Tables tb, const float2 *__restrict__ h,
                   int conj, float scale) {
-  using C = Cfg<L>;
-  extern __shared__ float2 sm[];
-  float2 *Cl[4] = {sm, sm + C::LPB, sm + 2 * C::LPB, sm + 3 * C::LPB};
-  const int y0 = blockIdx.x * 4;
-  load_rows<L>(Cl, in, L, y0, 4, 4);
-  __syncthreads();
-  fft4<L, false>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
+  using C = Cta<L, false>;
+  extern __shared__ float4 sm4[];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  float2 v[16];
+  ld_row<L>(v, in + (size_t)y * L, t);
+  fft<L, false>(v, x, t, tb.tw);
+  const float s = scale / L;
   if (conj)
-    mul_lines<L, true>(Cl, 4, h, scale / L);
+    mul_tab<L, true>(v, h, t);
   else
-    mul_lines<L, false>(Cl, 4, h, scale / L);
-  __syncthreads();
-  fft4<L, true>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-  store_rows<L>(Cl, out, L, y0, 4, 4, 1.0f);
+    mul_tab<L, false>(v, h, t);
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cscale(v[r], s);
+  fft<L, true>(v, x, t, tb.tw);
+  st_row<L>(v, out + (size_t)y * L, t);
 }
 
-// columns (4 / CTA): out (+)= scale * IFFT(h^(*) FFT(in)) along y
+// columns: out (+)= scale * IFFT(h^(*) FFT(in)) / L along y
 template <int L>
-__global__ void __launch_bounds__(Cfg<L>::NT, 1)
+__global__ void __launch_bounds__(512, 1)
     k_cols_filter(const float2 *__restrict__ in, float2 *__restrict__ out, Tables tb, const float2 *__restrict__ h,
                   int conj, float scale, int accumulate) {
-  using C = Cfg<L>;
-  extern __shared__ float2 sm[];
-  float2 *Cl[4] = {sm, sm + C::LPB, sm + 2 * C::LPB, sm + 3 * C::LPB};
-  const int x0 = blockIdx.x * 4;
-  load_cols4<L>(Cl, in, x0, 0, L, 0);
-  __syncthreads();
-  fft4<L, false>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
+  using C = Cta<L, true>;
+  constexpr int T = L / 16;
+  extern __shared__ float4 sm4[];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const int t = C::t(), col = blockIdx.x * C::G + C::g();
+  float2 v[16];
+  ld_col<L>(v, in + col, t);
+  fft<L, false>(v, x, t, tb.tw);
+  const float s = scale / L;
   if (conj)
-    mul_lines<L, true>(Cl, 4, h, scale / L);
+    mul_tab<L, true>(v, h, t);
   else
-    mul_lines<L, false>(Cl, 4, h, scale / L);
-  __syncthreads();
-  fft4<L, true>(Cl[0], Cl[1], Cl[2], Cl[3], tb.tw);
-  if (accumulate) {
-    for (int e = threadIdx.x; e < 2 * L; e += blockDim.x) {
-      int y = e >> 1, hh = e & 1;
-      float4 *p = reinterpret_cast<float4 *>(out + (size_t)y * L + x0 + 2 * hh);
-      float4 v = *p;
-      float2 a = Cl[2 * hh][P(y)], b = Cl[2 * hh + 1][P(y)];
-      *p = make_float4(v.x + a.x, v.y + a.y, v.z + b.x, v.w + b.y);
-    }
-  } else {
-    store_cols4<L>(Cl, out, x0, 0, L, 0, 1.0f);
+    mul_tab<L, false>(v, h, t);
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cscale(v[r], s);
+  fft<L, true>(v, x, t, tb.tw);
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    float2 *p = out + (size_t)(t + r * T) * L + col;
+    *p = accumulate ? cadd(*p, v[r]) : v[r];
   }
 }
 

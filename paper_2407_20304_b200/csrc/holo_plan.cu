@@ -34,11 +34,13 @@ struct holo_plan {
   double m0 = 0, p0 = 0, mt[HOLO_MAX_NZ]{}, zeta[HOLO_MAX_NZ]{}, zdet[HOLO_MAX_NZ]{}, omega[HOLO_MAX_NZ]{};
   uint32_t magmask = 0;
   // device tables
-  float2 *tw = nullptr, *hdet = nullptr, *homega = nullptr, *cin = nullptr, *cout = nullptr, *bke = nullptr,
-         *bko = nullptr, *wodd = nullptr, *ramps = nullptr, *href = nullptr;
+  float2 *tw = nullptr, *hdet = nullptr, *homega = nullptr, *cout = nullptr, *cwo = nullptr, *bke = nullptr,
+         *bko = nullptr, *wodd = nullptr, *cr = nullptr;
+  std::vector<std::complex<double>> cin_host;  // [nz][L] kappa (-1)^fbar e^{i pi mt fbar^2/L} / L
   // workspace
   float2 *T1 = nullptr, *Aw = nullptr, *W1 = nullptr, *V1 = nullptr, *T3 = nullptr, *G = nullptr, *QJ = nullptr;
   double *partF = nullptr, *partX3 = nullptr, *partQ = nullptr;
+  int nbx2 = 0, nbx3 = 0;  // CTAs of the X2 / X3 launches (partials per frame / per angle)
   size_t ws_bytes = 0;
   std::vector<void *> allocs;
   std::string err;
@@ -57,8 +59,8 @@ struct holo_plan {
 
   Tables tables() const {
     Tables t;
-    t.tw = tw; t.hdet = hdet; t.homega = homega; t.cin = cin; t.cout = cout; t.bke = bke; t.bko = bko;
-    t.wodd = wodd; t.ramps = ramps; t.href = href;
+    t.tw = reinterpret_cast<const float4 *>(tw); t.hdet = hdet; t.homega = homega; t.cout = cout; t.cwo = cwo;
+    t.bke = bke; t.bko = bko; t.wodd = wodd; t.cr = cr;
     return t;
   }
 };
@@ -132,11 +134,10 @@ void fft64(std::vector<cd> &a) {
   }
 }
 
-int first_radix(int L) {  // must match FftShape<L>: S16 = (log2 L - 1) / 4, F = L / 16^S16
-  int s16 = 0, lg = 0;
+int radix16_stages(int L) {  // must match Shape<L>: S16 = (log2 L - 1) / 4, F = L / 16^S16
+  int lg = 0;
   while ((1 << lg) < L) lg++;
-  s16 = (lg - 1) / 4;
-  return L >> (4 * s16);
+  return (lg - 1) / 4;
 }
 
 // transfer h_z[f] = exp(-i pi lambda z (fbar/(L p0))^2), phase reduced in cycles
@@ -152,18 +153,25 @@ std::vector<cd> transfer(int L, double lam, double p0, double z) {
 bool supported_L(int L) { return L == 128 || L == 256 || L == 512 || L == 1024 || L == 2048 || L == 4096; }
 
 template <int L>
+struct Smem {
+  static constexpr size_t ROWS = Cta<L, false>::XBYTES, COLS = Cta<L, true>::XBYTES;
+  static constexpr size_t ROWS_P = ROWS + Cta<L, false>::PRIV, COLS_P = COLS + Cta<L, true>::PRIV;
+};
+
+template <int L>
 void set_smem_attrs() {
-  const int s = (int)Cfg<L>::SMEM;
-  cudaFuncSetAttribute(k_x1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_y1<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_x2<L, X2_GRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_x2<L, X2_FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_x2<L, X2_ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_x2<L, X2_OBJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_y2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_x3<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_rows_filter<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
-  cudaFuncSetAttribute(k_cols_filter<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, s);
+  using S = Smem<L>;
+  auto a = [](const void *f, size_t s) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s); };
+  a((const void *)k_x1<L>, S::ROWS_P);
+  a((const void *)k_y1<L>, S::COLS_P);
+  a((const void *)k_x2<L, X2_GRAD>, S::ROWS);
+  a((const void *)k_x2<L, X2_FWD>, S::ROWS);
+  a((const void *)k_x2<L, X2_ADJ>, S::ROWS);
+  a((const void *)k_x2<L, X2_OBJ>, S::ROWS);
+  a((const void *)k_y2<L>, S::COLS_P);
+  a((const void *)k_x3<L>, S::ROWS_P);
+  a((const void *)k_rows_filter<L>, S::ROWS);
+  a((const void *)k_cols_filter<L>, S::COLS);
 }
 
 void set_attrs(int L) {
@@ -221,18 +229,19 @@ double fftf(int L) {  // 5 L log2 L flops per length-L complex FFT
 // ------------------------------------------------------------------ pass runners
 template <int L>
 struct Run {
-  static constexpr size_t SM = Cfg<L>::SMEM;
-  static constexpr int NT = Cfg<L>::NT;
+  using SM = Smem<L>;
+  static constexpr int NT = 512;
+  static constexpr int GR = Cta<L, false>::G, GC = Cta<L, true>::G;
   static constexpr double A = 8.0 * L * L;  // bytes of one L x L complex64 array
 
   static void rows_filter(holo_plan *p, const float2 *in, float2 *out, const float2 *h, int conj, float scale) {
     pbeg(p);
-    k_rows_filter<L><<<L / 4, NT, SM, p->stream>>>(in, out, p->tables(), h, conj, scale);
+    k_rows_filter<L><<<L / GR, NT, SM::ROWS, p->stream>>>(in, out, p->tables(), h, conj, scale);
     pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
   }
   static void cols_filter(holo_plan *p, const float2 *in, float2 *out, const float2 *h, int conj, float scale, int acc) {
     pbeg(p);
-    k_cols_filter<L><<<L / 4, NT, SM, p->stream>>>(in, out, p->tables(), h, conj, scale, acc);
+    k_cols_filter<L><<<L / GC, NT, SM::COLS, p->stream>>>(in, out, p->tables(), h, conj, scale, acc);
     pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 2.0 * L * fftf(L));
   }
 
@@ -271,7 +280,7 @@ struct Run {
     Tables tb = p->tables();
     const int N = p->N, nz = p->nz, K = p->K;
     const size_t LL = (size_t)L * L;
-    const int nbx2 = (N + 3) / 4;
+    const int nbx2 = (N + GR - 1) / GR;
     const double fl = fftf(L), rN = (double)N / L, NN8 = 8.0 * N * N;
     int nmag = 0;
     for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
@@ -282,7 +291,7 @@ struct Run {
       const bool need_fwd_chain = (mode != 2) || want_q;
       if (need_fwd_chain) {
         pbeg(p);
-        k_x1<L><<<L / 2, NT, SM, p->stream>>>(psik, p->T1, tb, k, nz, p->magmask);
+        k_x1<L><<<L / GR, NT, SM::ROWS_P, p->stream>>>(psik, p->T1, tb, k, nz, p->magmask);
         pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * (1 + 4 * nmag + (nz - nmag)));
       }
       for (int j = 0; j < nz; j++) {
@@ -294,40 +303,40 @@ struct Run {
           float2 *aout = want_q ? p->Aw : nullptr;
           float2 *w1 = (mode == 2) ? nullptr : p->W1;
           pbeg(p);
-          k_y1<L><<<L / 4, NT, SM, p->stream>>>(T1j, qjj, aout, w1, tb, k, j, nz, mag, N);
+          k_y1<L><<<L / GC, NT, SM::COLS_P, p->stream>>>(T1j, qjj, aout, w1, tb, k, j, nz, mag, N);
           pend(p, HOLO_PASS_Y1, A + (w1 ? A + rN * A : 0) + (aout ? A : 0),
                L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0)));
         }
         double *pf = p->partF + fr * nbx2;
         pbeg(p);
         if (mode == 1) {
-          k_x2<L, X2_FWD><<<nbx2, NT, SM, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, j, N);
+          k_x2<L, X2_FWD><<<nbx2, NT, SM::ROWS, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, j, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
           continue;
         }
         if (mode == 3) {
-          k_x2<L, X2_OBJ><<<nbx2, NT, SM, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, j, N);
+          k_x2<L, X2_OBJ><<<nbx2, NT, SM::ROWS, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, j, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8 / 2, N * fl * 2);
           continue;
         }
         if (mode == 0) {
-          k_x2<L, X2_GRAD><<<nbx2, NT, SM, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, j, N);
+          k_x2<L, X2_GRAD><<<nbx2, NT, SM::ROWS, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, j, N);
           pend(p, HOLO_PASS_X2, 2 * rN * A + NN8 / 2, N * fl * 4);
         } else {
-          k_x2<L, X2_ADJ><<<nbx2, NT, SM, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, j, N);
+          k_x2<L, X2_ADJ><<<nbx2, NT, SM::ROWS, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, j, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
         }
         float2 *Gj = want_q ? p->G + (size_t)j * LL : nullptr;
         float2 *T3j = gpsi ? p->T3 + (size_t)j * LL : nullptr;
         pbeg(p);
-        k_y2<L><<<L / 4, NT, SM, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, tb, k, j, nz, mag, N);
+        k_y2<L><<<L / GC, NT, SM::COLS_P, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, tb, k, j, nz, mag, N);
         pend(p, HOLO_PASS_Y2, rN * A + (Gj ? 3 * A : 0) + (T3j ? 2 * A : 0),
              L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0)));
       }
       if (gpsi && (mode == 0 || mode == 2)) {
         pbeg(p);
-        k_x3<L><<<L / 2, NT, SM, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
-                                               p->partX3 + (size_t)k * L, tb, k, nz, p->magmask, gscale);
+        k_x3<L><<<L / GR, NT, SM::ROWS_P, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
+                                               p->partX3 + (size_t)k * 2 * p->nbx3, tb, k, nz, p->magmask, gscale);
         pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
       }
     }
@@ -345,6 +354,28 @@ void dispatch_sweep(holo_plan *p, A... a) {
     case 2048: R<2048>::sweep(p, a...); break;
     case 4096: R<4096>::sweep(p, a...); break;
   }
+}
+
+// spectrum factor per (k, j, axis): cr[f] = cin_j[f] r_s[f] for magnified planes, r_s[f] / L at mt = 1,
+// r_s[f] = e^{-2 pi i fbar s / L} (O4 / O5; the shift precedes the magnification, reading C4)
+holo_status upload_cr(holo_plan *p, const double *s) {
+  const int L = p->L, nz = p->nz, K = p->K;
+  std::vector<float2> r((size_t)K * nz * 2 * L);
+  for (int k = 0; k < K; k++)
+    for (int j = 0; j < nz; j++) {
+      const bool mag = (p->magmask >> j) & 1u;
+      for (int ax = 0; ax < 2; ax++) {
+        const double sv = s[((size_t)k * nz + j) * 2 + ax];
+        float2 *dst = r.data() + (((size_t)k * nz + j) * 2 + ax) * L;
+        for (int f = 0; f < L; f++) {
+          cd v = expi2pi_frac(-(double)fbar(f, L) * sv / (double)L);
+          v = mag ? v * p->cin_host[(size_t)j * L + f] : v / (double)L;
+          dst[f] = make_float2((float)v.real(), (float)v.imag());
+        }
+      }
+    }
+  HC(cudaMemcpy(p->cr, r.data(), r.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  return HOLO_OK;
 }
 
 holo_status precheck(holo_plan *p) {
@@ -397,16 +428,21 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   holo_status s = HOLO_OK;
   const size_t LL = (size_t)L * L;
   auto A = [&](auto **ptr, size_t bytes) { if (s == HOLO_OK) s = dalloc(p, ptr, bytes); };
-  A(&p->tw, sizeof(float2) * L);
+  const int GR = 8192 / L;  // rows per CTA of the row kernels (Cta<L, false>::G)
+  p->nbx2 = (N + GR - 1) / GR;
+  p->nbx3 = L / GR;
+  const size_t Kc = (size_t)(K > 0 ? K : 1);
+  const int S16 = radix16_stages(L), F = L >> (4 * S16);
+  const size_t twrows = (size_t)F * (((size_t)1 << (4 * S16)) - 1) / 15;  // F (16^S16 - 1) / 15
+  A(&p->tw, sizeof(float2) * 4 * twrows);
   A(&p->hdet, sizeof(float2) * L * nz);
   A(&p->homega, sizeof(float2) * L * nz);
-  A(&p->cin, sizeof(float2) * L * nz);
   A(&p->cout, sizeof(float2) * L * nz);
+  A(&p->cwo, sizeof(float2) * L * nz);
   A(&p->bke, sizeof(float2) * L * nz);
   A(&p->bko, sizeof(float2) * L * nz);
   A(&p->wodd, sizeof(float2) * L);
-  A(&p->href, sizeof(float2) * L);
-  A(&p->ramps, sizeof(float2) * L * 2 * nz * (size_t)(K > 0 ? K : 1));
+  A(&p->cr, sizeof(float2) * L * 2 * nz * Kc);
   A(&p->T1, sizeof(float2) * LL * nz);
   A(&p->Aw, sizeof(float2) * LL);
   A(&p->W1, sizeof(float2) * (size_t)N * L);
@@ -414,22 +450,27 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   A(&p->T3, sizeof(float2) * LL * nz);
   A(&p->G, sizeof(float2) * LL * nz);
   A(&p->QJ, sizeof(float2) * LL * nz);
-  A(&p->partF, sizeof(double) * (size_t)(K > 0 ? K : 1) * nz * ((N + 3) / 4));
-  A(&p->partX3, sizeof(double) * (size_t)(K > 0 ? K : 1) * L);
+  A(&p->partF, sizeof(double) * Kc * nz * p->nbx2);
+  A(&p->partX3, sizeof(double) * Kc * 2 * p->nbx3);
   A(&p->partQ, sizeof(double) * 2 * 1184);
   if (s != HOLO_OK) { holo_plan_destroy(p); return s; }
   // ---- tables (fp64 -> fp32)
   {
-    const int F = first_radix(L);
+    // FFT stage twiddle rows: radix-16 stage with Ns = F 16^st holds, per m < Ns,
+    // (w^m, w^2m, w^4m, w^8m), w = exp(-2 pi i / (16 Ns))   (fft_engine.cuh)
     std::vector<cd> tw;
     for (int Ns = F; Ns < L; Ns *= 16)
-      for (int r = 1; r < 16; r++)
-        for (int m = 0; m < Ns; m++) tw.push_back(expi2pi_frac(-(double)(m * r) / (16.0 * Ns)));
-    tw.resize(L, cd(0, 0));
+      for (int m = 0; m < Ns; m++)
+        for (int e : {1, 2, 4, 8}) tw.push_back(expi2pi_frac(-(double)((long)m * e) / (16.0 * Ns)));
+    if (tw.size() != 4 * twrows) { holo_plan_destroy(p); return HOLO_EUNSUPPORTED; }
     if (s == HOLO_OK) s = upload(p, p->tw, tw);
-    std::vector<cd> hd, ho, ci, co, be, bo;
+    std::vector<cd> wo(L);
+    for (int i = 0; i < L; i++) wo[i] = expi2pi_frac(-(double)i / (2.0 * L));  // w[i] = e^{-i pi i / L}
+    std::vector<cd> hd, ho, co, cw, be, bo;
+    p->cin_host.clear();
     for (int j = 0; j < nz; j++) {
       auto h1 = transfer(L, g->wavelength, p->p0, p->zdet[j]);
+      for (auto &h : h1) h /= (double)L;  // the 1/L of the inverse DFT folded in
       auto h2 = transfer(L, g->wavelength, p->p0, p->omega[j]);
       hd.insert(hd.end(), h1.begin(), h1.end());
       ho.insert(ho.end(), h2.begin(), h2.end());
@@ -440,11 +481,13 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
         double v = mt * (double)fb;
         bool kap = v >= -(double)(L / 2) && v < (double)(L / 2);
         double cyc = std::fmod(mt * (double)(fb * fb), 2.0 * L) / (2.0 * L) + (fb & 1 ? 0.5 : 0.0);
-        ci.push_back(kap ? expi2pi_frac(cyc) / (double)L : cd(0, 0));
+        p->cin_host.push_back(kap ? expi2pi_frac(cyc) / (double)L : cd(0, 0));
       }
       for (int o = 0; o < L; o++) {
         long n = o - L / 2;
-        co.push_back(expi2pi_frac(std::fmod(mt * (double)(n * n), 2.0 * L) / (2.0 * L)));
+        cd c = expi2pi_frac(std::fmod(mt * (double)(n * n), 2.0 * L) / (2.0 * L));
+        co.push_back(c);
+        cw.push_back(c * std::conj(wo[o]));
       }
       // b[d] = exp(-i pi mt d^2 / L), |d| < L, on a 2L cycle; Bhat = FFT_2L(b) / (2L)
       std::vector<cd> b(2 * L, cd(0, 0));
@@ -461,16 +504,15 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
     }
     if (s == HOLO_OK) s = upload(p, p->hdet, hd);
     if (s == HOLO_OK) s = upload(p, p->homega, ho);
-    if (s == HOLO_OK) s = upload(p, p->cin, ci);
     if (s == HOLO_OK) s = upload(p, p->cout, co);
+    if (s == HOLO_OK) s = upload(p, p->cwo, cw);
     if (s == HOLO_OK) s = upload(p, p->bke, be);
     if (s == HOLO_OK) s = upload(p, p->bko, bo);
-    std::vector<cd> wo(L);
-    for (int i = 0; i < L; i++) wo[i] = expi2pi_frac(-(double)i / (2.0 * L));
     if (s == HOLO_OK) s = upload(p, p->wodd, wo);
-    if (s == HOLO_OK) s = upload(p, p->href, transfer(L, g->wavelength, p->p0, p->zeta[0]));
-    std::vector<cd> one((size_t)L * 2 * nz * (K > 0 ? K : 1), cd(1, 0));
-    if (s == HOLO_OK) s = upload(p, p->ramps, one);
+  }
+  if (s == HOLO_OK && K > 0) {  // zero shifts until holo_set_shifts
+    std::vector<double> zero((size_t)K * nz * 2, 0.0);
+    s = upload_cr(p, zero.data());
   }
   if (s != HOLO_OK) { holo_plan_destroy(p); return s; }
   *out = p;
@@ -533,19 +575,7 @@ holo_status holo_set_shifts(holo_plan *p, const double *s) {
   const int L = p->L, nz = p->nz, K = p->K;
   for (size_t i = 0; i < (size_t)K * nz * 2; i++)
     if (!std::isfinite(s[i]) || std::fabs(s[i]) >= L / 2) return fail(p, HOLO_EINVAL, "shift not finite or >= npad/2");
-  std::vector<float2> r((size_t)K * nz * 2 * L);
-  for (int k = 0; k < K; k++)
-    for (int j = 0; j < nz; j++)
-      for (int ax = 0; ax < 2; ax++) {
-        const double sv = s[((size_t)k * nz + j) * 2 + ax];
-        float2 *dst = r.data() + (((size_t)k * nz + j) * 2 + ax) * L;
-        for (int f = 0; f < L; f++) {
-          cd v = expi2pi_frac(-(double)fbar(f, L) * sv / (double)L);  // r_s[f] = e^{-2 pi i fbar s / L}
-          dst[f] = make_float2((float)v.real(), (float)v.imag());
-        }
-      }
-  HC(cudaMemcpy(p->ramps, r.data(), r.size() * sizeof(float2), cudaMemcpyHostToDevice));
-  return HOLO_OK;
+  return upload_cr(p, s);
 }
 
 holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
@@ -593,11 +623,11 @@ holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float 
                       (float2 *)nullptr, (const float2 *)eta_psi_prev, obj ? nullptr : (float2 *)grad_psi,
                       obj ? nullptr : (float2 *)grad_q_part, 2.0f, !obj && grad_q_part != nullptr);
   pbeg(p);
-  k_reduce<<<1, 1024, 0, p->stream>>>(p->partF, (size_t)K * nz * ((N + 3) / 4), 1, sc, 0);
+  k_reduce<<<1, 1024, 0, p->stream>>>(p->partF, (size_t)K * nz * p->nbx2, 1, sc, 0);
   pend(p, HOLO_PASS_REDUCE, 8.0 * K * nz * ((N + 3) / 4), 0);
   if (!obj && grad_psi) {
     pbeg(p);
-    k_reduce<<<1, 1024, 0, p->stream>>>(p->partX3, (size_t)K * (L / 2), 2, sc + 1, 0);
+    k_reduce<<<1, 1024, 0, p->stream>>>(p->partX3, (size_t)K * p->nbx3, 2, sc + 1, 0);
     pend(p, HOLO_PASS_REDUCE, 8.0 * K * L, 0);
   }
   return postcheck(p);
