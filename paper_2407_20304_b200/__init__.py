@@ -22,7 +22,7 @@ HOLO_ACCUMULATE_Q = 1
 HOLO_OBJECTIVE_ONLY = 2
 HOLO_MAX_NZ = 8
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("HOLO_LIB", _build.LIB)  # HOLO_LIB: a tuning-variant build of the same sources
 if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"libholo.so not found at {LIB_PATH}: build it with `python paper_2407_20304_b200/_build.py` "

@@ -24,17 +24,22 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Compile libholo.so; `defines` (e.g. ["-DHOLO_NT_ROWS=256"]) and `out` build tuning variants."""
+    if not force and out == LIB and not defines and up_to_date():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [NVCC] + FLAGS + [os.path.join(CSRC, "holo_plan.cu"), "-o", tmp]
+    tmp = out + ".tmp%d" % os.getpid()
+    cmd = [NVCC] + FLAGS + list(defines) + [os.path.join(CSRC, "holo_plan.cu"), "-o", tmp]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=LIB)
+    a, defines = ap.parse_known_args()  # the rest: -DNAME=VALUE tuning knobs
+    print(build(force=True, verbose=True, out=a.out, defines=defines))

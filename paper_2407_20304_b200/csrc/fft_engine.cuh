@@ -31,6 +31,16 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Build knobs (compile-time, for the engine microbenchmark tools/fftbench.cu):
+//   HOLO_TW_FULL   1: load all 15 stage twiddles from a [stage][m][16] table instead of 4 powers
+//   HOLO_SINGLE_BUF 1: one exchange buffer per line, two barriers per exchange
+#ifndef HOLO_TW_FULL
+#define HOLO_TW_FULL 0
+#endif
+#ifndef HOLO_SINGLE_BUF
+#define HOLO_SINGLE_BUF 0
+#endif
+
 namespace holo {
 
 __device__ __forceinline__ int P(int i) { return i + (i >> 4); }
@@ -135,9 +145,14 @@ struct Xch {
   int par;
   int stride;
   __device__ __forceinline__ float2 *next() {
+#if HOLO_SINGLE_BUF
+    __syncthreads();  // previous readers of the single buffer are done
+    return b;
+#else
     float2 *p = par ? b + stride : b;
     par ^= 1;
     return p;
+#endif
   }
 };
 
@@ -150,6 +165,18 @@ __device__ __forceinline__ void r16_stage(float2 (&v)[16], Xch &x, const int t, 
   constexpr int Ns = S::F * pow16(ST);
   constexpr int ROW0 = S::F * (pow16(ST) - 1) / 15;
   const int m = t & (Ns - 1);
+#if HOLO_TW_FULL
+  {
+    // full table: rows of 8 float4 = 16 float2 (entry 0 unused) per (stage, m)
+    const float4 *row = tw + 8 * (ROW0 + m);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const float4 a = __ldg(row + q);
+      if (q > 0) twmul<INV>(v[2 * q], make_float2(a.x, a.y));
+      twmul<INV>(v[2 * q + 1], make_float2(a.z, a.w));
+    }
+  }
+#else
   {
     const float4 a = __ldg(tw + 2 * (ROW0 + m)), b = __ldg(tw + 2 * (ROW0 + m) + 1);
     const float2 w1 = make_float2(a.x, a.y), w2 = make_float2(a.z, a.w), w4 = make_float2(b.x, b.y),
@@ -171,6 +198,7 @@ __device__ __forceinline__ void r16_stage(float2 (&v)[16], Xch &x, const int t, 
     twmul<INV>(v[14], cmul(w6, w8));
     twmul<INV>(v[15], cmul(w7, w8));
   }
+#endif
   dft_reg<16, INV>(v);
   if constexpr (ST + 1 < S::S16) {
     float2 *buf = x.next();

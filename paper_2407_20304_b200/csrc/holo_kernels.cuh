@@ -40,26 +40,33 @@ struct Tables {
   const float2 *cr;     // [K][nz][2][L] spectrum factor per (k, j, axis): mag: cin r_s, else r_s / L
 };
 
-// CTA geometry: NT = 512 threads, G = NT / T lines.  ROWS kernels map threads
-// t-major (g = tid / T) so a warp reads one row contiguously; COLS kernels map
-// them g-major (g = tid % G) so a warp reads G adjacent columns per row.
-template <int L, bool COLS>
+// CTA geometry: NT threads, G = NT / T lines per CTA, threads mapped g-major
+// (g = tid % G, t = tid / G): one warp covers G adjacent lines (rows or columns)
+// at 32/G consecutive positions, which is what the P2 layout below needs for full
+// 32-byte sectors in both directions.
+template <int L, int NT_ = 512>
 struct Cta {
   static constexpr int T = Shape<L>::T;
-  static constexpr int NT = 512;
+  static constexpr int NT = NT_;
   static constexpr int G = NT / T;
   static constexpr int LP = Shape<L>::LP;
   static constexpr int LPB = (LP + 15) / 16 * 16;  // one buffer, 16-float2 aligned
   // per-group stride (two buffers) skewed so that the groups sharing a 16-lane
   // phase land on distinct banks
-  static constexpr int SKEW = COLS ? (G <= 16 ? 16 / G : 1) : (T >= 16 ? 0 : 8);
+  static constexpr int SKEW = G <= 16 ? 16 / G : 1;
   static constexpr int GS = 2 * LPB + SKEW;
   static constexpr size_t XBYTES = sizeof(float2) * (size_t)GS * G;
   static constexpr size_t PRIV = sizeof(float2) * 16 * NT;  // one thread-private line
-  __device__ __forceinline__ static int g() { return COLS ? threadIdx.x % G : threadIdx.x / T; }
-  __device__ __forceinline__ static int t() { return COLS ? threadIdx.x / G : threadIdx.x % T; }
+  __device__ __forceinline__ static int g() { return threadIdx.x % G; }
+  __device__ __forceinline__ static int t() { return threadIdx.x / G; }
   __device__ __forceinline__ static Xch xch(float2 *sm) { return Xch{sm + (size_t)g() * GS, 0, LPB}; }
 };
+
+// P2 layout ("column-pair interleaved") of an R x L complex64 workspace array:
+// element (y, x) at ((x >> 1) R + y) 2 + (x & 1).  A column pair is one contiguous
+// block of 16 R bytes (column passes stream it like a row); two adjacent rows of a
+// row pass fill whole 32-byte sectors.
+__device__ __forceinline__ size_t p2(int y, int x, int R) { return ((size_t)(x >> 1) * R + y) * 2 + (x & 1); }
 
 // thread-private spill slot of 16 float2 (conflict free: consecutive threads, consecutive slots)
 template <int NT>

@@ -1,31 +1,59 @@
 // holo_passes.cuh -- the five line-pass kernels (X1, Y1, X2, Y2, X3), the
 // propagation filters for q_j / g_q, reductions and the CG pointwise step.
 //
-// All line kernels: 512 threads, G = 512 / (L/16) lines per CTA, one CTA per SM
-// at L = 4096 (<= 128 registers; exchange buffers + one thread-private line in
-// shared memory).
+// Line kernels: 512 threads, G = 512 / (L/16) lines per CTA (g-major), <= 128
+// registers per thread; shared memory = double-buffered exchange space + (Bluestein
+// kernels) one thread-private line.  Workspace arrays (T1, Aw, W1, V1, T3, G, QJ)
+// are in the P2 layout (holo_kernels.cuh); the caller's arrays (psi, q, w, sqrt_d,
+// grad, eta) are row-major.
 #pragma once
 #include "holo_kernels.cuh"
 
 namespace holo {
 
+constexpr int NT = 512;
+template <int L>
+using CtaK = Cta<L, NT>;
+
 enum { X2_GRAD = 0, X2_FWD = 1, X2_ADJ = 2, X2_OBJ = 3 };
 
-template <int L, bool COLS>
+template <int L>
 __device__ __forceinline__ float2 *priv_base(float2 *sm) {
-  return sm + Cta<L, COLS>::XBYTES / sizeof(float2);
+  return sm + CtaK<L>::XBYTES / sizeof(float2);
+}
+
+// layout-S line access of a P2 array with R rows: row y (x = t + T r) / column x (y = t + T r)
+template <int L>
+__device__ __forceinline__ void ld_p2_row(float2 (&v)[16], const float2 *__restrict__ a, int y, int R, int t) {
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = ldg2(a + p2(y, t + r * (L / 16), R));
+}
+template <int L>
+__device__ __forceinline__ void st_p2_row(const float2 (&v)[16], float2 *__restrict__ a, int y, int R, int t) {
+#pragma unroll
+  for (int r = 0; r < 16; r++) a[p2(y, t + r * (L / 16), R)] = v[r];
+}
+template <int L>
+__device__ __forceinline__ void ld_p2_col(float2 (&v)[16], const float2 *__restrict__ a, int x, int R, int t) {
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = ldg2(a + p2(t + r * (L / 16), x, R));
+}
+template <int L>
+__device__ __forceinline__ void st_p2_col(const float2 (&v)[16], float2 *__restrict__ a, int x, int R, int t) {
+#pragma unroll
+  for (int r = 0; r < 16; r++) a[p2(t + r * (L / 16), x, R)] = v[r];
 }
 
 // ----------------------------------------------------------------------------- X1
-// rows of psi_k:  X = FFT(psi row) (kept thread-private); per j: T1_j row = M_{1/mt_j} S_{sx} psi row
+// rows of psi_k (row-major):  X = FFT(psi row) (kept thread-private); per j: T1_j row = M_{1/mt_j} S_{sx} psi row
 template <int L>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(NT, 1)
     k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1, Tables tb, int k, int nz, uint32_t magmask) {
-  using C = Cta<L, false>;
+  using C = CtaK<L>;
   extern __shared__ float4 sm4[];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
-  const Priv<512> X{priv_base<L, false>(sm)};
+  const Priv<NT> X{priv_base<L>(sm)};
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 v[16];
   ld_row<L>(v, psi_k + (size_t)y * L, t);
@@ -41,27 +69,27 @@ __global__ void __launch_bounds__(512, 1)
       for (int r = 0; r < 16; r++) v[r] = cmul(X[r], ldg2(cr + t + r * (L / 16)));
       fft<L, true>(v, x, t, tb.tw);
     }
-    st_row<L>(v, T1 + (size_t)j * L * L + (size_t)y * L, t);
+    st_p2_row<L>(v, T1 + (size_t)j * L * L, y, L, t);
   }
 }
 
 // ----------------------------------------------------------------------------- Y1
 // columns of T1_j:  a = M_{1/mt_j} S_{sy} (column);  optionally store a;
-// optionally  W1 = rows [o, o+N) of D_y(q_j . a)
+// optionally  W1 = rows [o, o+N) of D_y(q_j . a)   (W1: P2 with N rows)
 template <int L>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(NT, 1)
     k_y1(const float2 *__restrict__ T1j, const float2 *__restrict__ qj, float2 *__restrict__ Aout,
          float2 *__restrict__ W1, Tables tb, int k, int j, int nz, int mag, int N) {
-  using C = Cta<L, true>;
+  using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
-  const Priv<512> X{priv_base<L, true>(sm)};
+  const Priv<NT> X{priv_base<L>(sm)};
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
   const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 1) * L;
   float2 v[16];
-  ld_col<L>(v, T1j + col, t);
+  ld_p2_col<L>(v, T1j, col, L, t);
   fft<L, false>(v, x, t, tb.tw);
   if (mag) {
 #pragma unroll
@@ -71,10 +99,10 @@ __global__ void __launch_bounds__(512, 1)
     mul_tab<L, false>(v, cr, t);
     fft<L, true>(v, x, t, tb.tw);
   }
-  if (Aout) st_col<L>(v, Aout + col, t);
+  if (Aout) st_p2_col<L>(v, Aout, col, L, t);
   if (W1) {
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + (size_t)(t + r * T) * L + col));
+    for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + p2(t + r * T, col, L)));
     fft<L, false>(v, x, t, tb.tw);
     mul_tab<L, false>(v, tb.hdet + (size_t)j * L, t);
     fft<L, true>(v, x, t, tb.tw);
@@ -82,21 +110,21 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const int row = t + r * T - o;
-      if (row >= 0 && row < N) W1[(size_t)row * L + col] = v[r];
+      if (row >= 0 && row < N) W1[p2(row, col, N)] = v[r];
     }
   }
 }
 
 // ----------------------------------------------------------------------------- X2
-// rows y < N.  GRAD: W1 row -> D_x, crop, residual (+F), pad, D_x^* -> V1
-//              FWD : W1 row -> D_x, crop -> w frame [N][N]
-//              ADJ : y frame row -> pad, D_x^* -> V1
+// rows y < N.  GRAD: W1 row -> D_x, crop, residual (+F), pad, D_x^* -> V1   (W1, V1: P2, N rows)
+//              FWD : W1 row -> D_x, crop -> w frame [N][N] (row-major)
+//              ADJ : y frame row (row-major) -> pad, D_x^* -> V1
 //              OBJ : W1 row -> D_x, crop, F only
 template <int L, int MODE>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(NT, 1)
     k_x2(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
          double *__restrict__ partial, Tables tb, int j, int N) {
-  using C = Cta<L, false>;
+  using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
   __shared__ double red[32];
@@ -109,7 +137,7 @@ __global__ void __launch_bounds__(512, 1)
   float2 v[16];
   if (MODE != X2_ADJ) {
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = act ? ldg2(in + (size_t)y * L + t + r * T) : make_float2(0.f, 0.f);
+    for (int r = 0; r < 16; r++) v[r] = act ? ldg2(in + p2(y, t + r * T, N)) : make_float2(0.f, 0.f);
     fft<L, false>(v, x, t, tb.tw);
     mul_tab<L, false>(v, h, t);
     fft<L, true>(v, x, t, tb.tw);
@@ -133,7 +161,7 @@ __global__ void __launch_bounds__(512, 1)
         const float m = sqrtf(v[r].x * v[r].x + v[r].y * v[r].y);
         const float dm = m - d;
         acc += (double)(dm * dm);
-        const float f = m > 0.f ? 1.0f - d / m : 0.f;  // rho = w - d w/|w|, 0 at w = 0 (C7)
+        const float f = m > 0.f ? 1.0f - __fdividef(d, m) : 0.f;  // rho = w - d w/|w|, 0 at w = 0 (C7)
         w = cscale(v[r], f);
       }
       v[r] = w;
@@ -151,28 +179,28 @@ __global__ void __launch_bounds__(512, 1)
   fft<L, false>(v, x, t, tb.tw);
   mul_tab<L, true>(v, h, t);
   fft<L, true>(v, x, t, tb.tw);
-  if (act) st_row<L>(v, out + (size_t)y * L, t);
+  if (act) st_p2_row<L>(v, out, y, N, t);
 }
 
 // ----------------------------------------------------------------------------- Y2
 // columns:  v = D_y^* pad(V1 col);  G_j += conj(a) v;  T3_j = (M S)_y^*(conj(q_j) v)
 template <int L>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(NT, 1)
     k_y2(const float2 *__restrict__ V1, const float2 *__restrict__ a, const float2 *__restrict__ qj,
          float2 *__restrict__ Gj, float2 *__restrict__ T3j, Tables tb, int k, int j, int nz, int mag, int N) {
-  using C = Cta<L, true>;
+  using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
-  const Priv<512> Y{priv_base<L, true>(sm)};
+  const Priv<NT> Y{priv_base<L>(sm)};
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
   const int o = (L - N) / 2;
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; r++) {
     const int row = t + r * T - o;
-    v[r] = (row >= 0 && row < N) ? ldg2(V1 + (size_t)row * L + col) : make_float2(0.f, 0.f);
+    v[r] = (row >= 0 && row < N) ? ldg2(V1 + p2(row, col, N)) : make_float2(0.f, 0.f);
   }
   fft<L, false>(v, x, t, tb.tw);
   mul_tab<L, true>(v, tb.hdet + (size_t)j * L, t);
@@ -180,13 +208,13 @@ __global__ void __launch_bounds__(512, 1)
   if (Gj) {
 #pragma unroll
     for (int r = 0; r < 16; r++) {
-      const size_t gi = (size_t)(t + r * T) * L + col;
+      const size_t gi = p2(t + r * T, col, L);
       Gj[gi] = cadd(Gj[gi], cmulc(v[r], ldg2(a + gi)));
     }
   }
   if (!T3j) return;
 #pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + (size_t)(t + r * T) * L + col));
+  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));
   const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 1) * L;
   if (mag) {
 #pragma unroll
@@ -197,32 +225,32 @@ __global__ void __launch_bounds__(512, 1)
     mul_tab<L, true>(v, cr, t);
   }
   fft<L, true>(v, x, t, tb.tw);
-  st_col<L>(v, T3j + col, t);
+  st_p2_col<L>(v, T3j, col, L, t);
 }
 
 // ----------------------------------------------------------------------------- X3
 // rows: g_k row = scale * IFFT( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3_j row;
-// partial[blk][0] = sum |g|^2, partial[blk][1] = sum Re(g conj(eta))
+// partial[blk][0] = sum |g|^2, partial[blk][1] = sum Re(g conj(eta))   (g, eta row-major)
 template <int L>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(NT, 1)
     k_x3(const float2 *__restrict__ T3, const float2 *__restrict__ eta, float2 *__restrict__ g,
          double *__restrict__ partial, Tables tb, int k, int nz, uint32_t magmask, float scale) {
-  using C = Cta<L, false>;
+  using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
   __shared__ double red[32];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
-  const Priv<512> W{priv_base<L, false>(sm)};
+  const Priv<NT> W{priv_base<L>(sm)};
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 v[16];
   for (int j = 0; j < nz; j++) {
-    const float2 *row = T3 + (size_t)j * L * L + (size_t)y * L;
+    const float2 *T3j = T3 + (size_t)j * L * L;
     const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 0) * L;
     if ((magmask >> j) & 1u) {
-      mag_adj<L>(v, [&](int r) { return ldg2(row + t + r * T); }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
+      mag_adj<L>(v, [&](int r) { return ldg2(T3j + p2(y, t + r * T, L)); }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
     } else {
-      ld_row<L>(v, row, t);
+      ld_p2_row<L>(v, T3j, y, L, t);
       fft<L, false>(v, x, t, tb.tw);
       mul_tab<L, true>(v, cr, t);
     }
@@ -262,44 +290,24 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
-// ------------------------------------------------------------------ filters
-// rows: out = scale * IFFT(h^(*) FFT(in)) / L along x
-template <int L>
-__global__ void __launch_bounds__(512, 1)
+// ------------------------------------------------------------------ filters (q_j, g_q)
+// rows: out = scale/L * IFFT(h^(*) FFT(in)) along x.
+// IN_P2 / OUT_P2: layout of in / out (else row-major); ACC: out += ...
+template <int L, bool IN_P2, bool OUT_P2, bool ACC>
+__global__ void __launch_bounds__(NT, 1)
     k_rows_filter(const float2 *__restrict__ in, float2 *__restrict__ out, Tables tb, const float2 *__restrict__ h,
                   int conj, float scale) {
-  using C = Cta<L, false>;
+  using C = CtaK<L>;
+  constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 v[16];
-  ld_row<L>(v, in + (size_t)y * L, t);
-  fft<L, false>(v, x, t, tb.tw);
-  const float s = scale / L;
-  if (conj)
-    mul_tab<L, true>(v, h, t);
+  if (IN_P2)
+    ld_p2_row<L>(v, in, y, L, t);
   else
-    mul_tab<L, false>(v, h, t);
-#pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = cscale(v[r], s);
-  fft<L, true>(v, x, t, tb.tw);
-  st_row<L>(v, out + (size_t)y * L, t);
-}
-
-// columns: out (+)= scale * IFFT(h^(*) FFT(in)) / L along y
-template <int L>
-__global__ void __launch_bounds__(512, 1)
-    k_cols_filter(const float2 *__restrict__ in, float2 *__restrict__ out, Tables tb, const float2 *__restrict__ h,
-                  int conj, float scale, int accumulate) {
-  using C = Cta<L, true>;
-  constexpr int T = L / 16;
-  extern __shared__ float4 sm4[];
-  float2 *sm = reinterpret_cast<float2 *>(sm4);
-  Xch x = C::xch(sm);
-  const int t = C::t(), col = blockIdx.x * C::G + C::g();
-  float2 v[16];
-  ld_col<L>(v, in + col, t);
+    ld_row<L>(v, in + (size_t)y * L, t);
   fft<L, false>(v, x, t, tb.tw);
   const float s = scale / L;
   if (conj)
@@ -311,8 +319,45 @@ __global__ void __launch_bounds__(512, 1)
   fft<L, true>(v, x, t, tb.tw);
 #pragma unroll
   for (int r = 0; r < 16; r++) {
-    float2 *p = out + (size_t)(t + r * T) * L + col;
-    *p = accumulate ? cadd(*p, v[r]) : v[r];
+    float2 *p = out + (OUT_P2 ? p2(y, t + r * T, L) : (size_t)y * L + t + r * T);
+    *p = ACC ? cadd(*p, v[r]) : v[r];
+  }
+}
+
+// columns of a P2 array, in place allowed: out = scale/L * IFFT(h^(*) FFT(in)) along y
+template <int L>
+__global__ void __launch_bounds__(NT, 1)
+    k_cols_filter(const float2 *__restrict__ in, float2 *__restrict__ out, Tables tb, const float2 *__restrict__ h,
+                  int conj, float scale) {
+  using C = CtaK<L>;
+  extern __shared__ float4 sm4[];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const int t = C::t(), col = blockIdx.x * C::G + C::g();
+  float2 v[16];
+  ld_p2_col<L>(v, in, col, L, t);
+  fft<L, false>(v, x, t, tb.tw);
+  const float s = scale / L;
+  if (conj)
+    mul_tab<L, true>(v, h, t);
+  else
+    mul_tab<L, false>(v, h, t);
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cscale(v[r], s);
+  fft<L, true>(v, x, t, tb.tw);
+  st_p2_col<L>(v, out, col, L, t);
+}
+
+// layout conversion (plane without propagation, omega_j = 0):  P2 <-> row-major, out (+)= scale * in
+__global__ void k_p2_convert(const float2 *__restrict__ in, float2 *__restrict__ out, int L, int to_p2, float scale,
+                             int accumulate) {
+  const size_t n = (size_t)L * L;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / L), xx = (int)(i % L);
+    const size_t pi = p2(y, xx, L);
+    const size_t si = to_p2 ? i : pi, di = to_p2 ? pi : i;
+    const float2 v = cscale(in[si], scale);
+    out[di] = accumulate ? cadd(out[di], v) : v;
   }
 }
 

@@ -154,24 +154,26 @@ bool supported_L(int L) { return L == 128 || L == 256 || L == 512 || L == 1024 |
 
 template <int L>
 struct Smem {
-  static constexpr size_t ROWS = Cta<L, false>::XBYTES, COLS = Cta<L, true>::XBYTES;
-  static constexpr size_t ROWS_P = ROWS + Cta<L, false>::PRIV, COLS_P = COLS + Cta<L, true>::PRIV;
+  static constexpr size_t X = CtaK<L>::XBYTES;            // exchange space only
+  static constexpr size_t XP = X + CtaK<L>::PRIV;         // + one thread-private line (Bluestein kernels)
 };
 
 template <int L>
 void set_smem_attrs() {
   using S = Smem<L>;
   auto a = [](const void *f, size_t s) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s); };
-  a((const void *)k_x1<L>, S::ROWS_P);
-  a((const void *)k_y1<L>, S::COLS_P);
-  a((const void *)k_x2<L, X2_GRAD>, S::ROWS);
-  a((const void *)k_x2<L, X2_FWD>, S::ROWS);
-  a((const void *)k_x2<L, X2_ADJ>, S::ROWS);
-  a((const void *)k_x2<L, X2_OBJ>, S::ROWS);
-  a((const void *)k_y2<L>, S::COLS_P);
-  a((const void *)k_x3<L>, S::ROWS_P);
-  a((const void *)k_rows_filter<L>, S::ROWS);
-  a((const void *)k_cols_filter<L>, S::COLS);
+  a((const void *)k_x1<L>, S::XP);
+  a((const void *)k_y1<L>, S::XP);
+  a((const void *)k_x2<L, X2_GRAD>, S::X);
+  a((const void *)k_x2<L, X2_FWD>, S::X);
+  a((const void *)k_x2<L, X2_ADJ>, S::X);
+  a((const void *)k_x2<L, X2_OBJ>, S::X);
+  a((const void *)k_y2<L>, S::XP);
+  a((const void *)k_x3<L>, S::XP);
+  a((const void *)k_rows_filter<L, false, true, false>, S::X);
+  a((const void *)k_rows_filter<L, true, false, false>, S::X);
+  a((const void *)k_rows_filter<L, true, false, true>, S::X);
+  a((const void *)k_cols_filter<L>, S::X);
 }
 
 void set_attrs(int L) {
@@ -230,46 +232,48 @@ double fftf(int L) {  // 5 L log2 L flops per length-L complex FFT
 template <int L>
 struct Run {
   using SM = Smem<L>;
-  static constexpr int NT = 512;
-  static constexpr int GR = Cta<L, false>::G, GC = Cta<L, true>::G;
+  static constexpr int G = CtaK<L>::G;
   static constexpr double A = 8.0 * L * L;  // bytes of one L x L complex64 array
 
-  static void rows_filter(holo_plan *p, const float2 *in, float2 *out, const float2 *h, int conj, float scale) {
-    pbeg(p);
-    k_rows_filter<L><<<L / GR, NT, SM::ROWS, p->stream>>>(in, out, p->tables(), h, conj, scale);
-    pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
-  }
-  static void cols_filter(holo_plan *p, const float2 *in, float2 *out, const float2 *h, int conj, float scale, int acc) {
-    pbeg(p);
-    k_cols_filter<L><<<L / GC, NT, SM::COLS, p->stream>>>(in, out, p->tables(), h, conj, scale, acc);
-    pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 2.0 * L * fftf(L));
-  }
-
+  // q_j = P_{omega_j} q (O6): row-major q -> P2 QJ_j
   static void qj(holo_plan *p, const float2 *q) {
+    const Tables tb = p->tables();
     for (int j = 0; j < p->nz; j++) {
       float2 *dst = p->QJ + (size_t)j * L * L;
+      pbeg(p);
       if (p->omega[j] == 0.0) {
-        cudaMemcpyAsync(dst, q, sizeof(float2) * L * L, cudaMemcpyDeviceToDevice, p->stream);
+        k_p2_convert<<<1184, 256, 0, p->stream>>>(q, dst, L, 1, 1.0f, 0);
+        pend(p, HOLO_PASS_FILTER, 2 * A, 0);
         continue;
       }
-      rows_filter(p, q, dst, p->homega + j * L, 0, 1.0f);
-      cols_filter(p, dst, dst, p->homega + j * L, 0, 1.0f, 0);
+      k_rows_filter<L, false, true, false><<<L / G, NT, SM::X, p->stream>>>(q, dst, tb, p->homega + j * L, 0, 1.0f);
+      pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
+      pbeg(p);
+      k_cols_filter<L><<<L / G, NT, SM::X, p->stream>>>(dst, dst, tb, p->homega + j * L, 0, 1.0f);
+      pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
     }
   }
 
-  // g_q (+)= scale * sum_j P_{-omega_j} G_j
+  // g_q (+)= scale * sum_j P_{-omega_j} G_j   (G_j P2 -> row-major out)
   static void gq(holo_plan *p, float2 *out, float scale, bool accumulate) {
+    const Tables tb = p->tables();
     for (int j = 0; j < p->nz; j++) {
       float2 *Gj = p->G + (size_t)j * L * L;
-      int acc = (accumulate || j > 0) ? 1 : 0;
+      const bool acc = accumulate || j > 0;
+      pbeg(p);
       if (p->omega[j] == 0.0) {
-        pbeg(p);
-        k_scale_add<<<1184, 256, 0, p->stream>>>(Gj, out, (size_t)L * L, scale, acc);
+        k_p2_convert<<<1184, 256, 0, p->stream>>>(Gj, out, L, 0, scale, acc ? 1 : 0);
         pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 0);
         continue;
       }
-      rows_filter(p, Gj, Gj, p->homega + j * L, 1, 1.0f);
-      cols_filter(p, Gj, out, p->homega + j * L, 1, scale, acc);
+      k_cols_filter<L><<<L / G, NT, SM::X, p->stream>>>(Gj, Gj, tb, p->homega + j * L, 1, 1.0f);
+      pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
+      pbeg(p);
+      if (acc)
+        k_rows_filter<L, true, false, true><<<L / G, NT, SM::X, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale);
+      else
+        k_rows_filter<L, true, false, false><<<L / G, NT, SM::X, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale);
+      pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 2.0 * L * fftf(L));
     }
   }
 
@@ -280,7 +284,7 @@ struct Run {
     Tables tb = p->tables();
     const int N = p->N, nz = p->nz, K = p->K;
     const size_t LL = (size_t)L * L;
-    const int nbx2 = (N + GR - 1) / GR;
+    const int nbx2 = (N + G - 1) / G;
     const double fl = fftf(L), rN = (double)N / L, NN8 = 8.0 * N * N;
     int nmag = 0;
     for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
@@ -291,7 +295,7 @@ struct Run {
       const bool need_fwd_chain = (mode != 2) || want_q;
       if (need_fwd_chain) {
         pbeg(p);
-        k_x1<L><<<L / GR, NT, SM::ROWS_P, p->stream>>>(psik, p->T1, tb, k, nz, p->magmask);
+        k_x1<L><<<L / G, NT, SM::XP, p->stream>>>(psik, p->T1, tb, k, nz, p->magmask);
         pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * (1 + 4 * nmag + (nz - nmag)));
       }
       for (int j = 0; j < nz; j++) {
@@ -303,39 +307,39 @@ struct Run {
           float2 *aout = want_q ? p->Aw : nullptr;
           float2 *w1 = (mode == 2) ? nullptr : p->W1;
           pbeg(p);
-          k_y1<L><<<L / GC, NT, SM::COLS_P, p->stream>>>(T1j, qjj, aout, w1, tb, k, j, nz, mag, N);
+          k_y1<L><<<L / G, NT, SM::XP, p->stream>>>(T1j, qjj, aout, w1, tb, k, j, nz, mag, N);
           pend(p, HOLO_PASS_Y1, A + (w1 ? A + rN * A : 0) + (aout ? A : 0),
                L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0)));
         }
         double *pf = p->partF + fr * nbx2;
         pbeg(p);
         if (mode == 1) {
-          k_x2<L, X2_FWD><<<nbx2, NT, SM::ROWS, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, j, N);
+          k_x2<L, X2_FWD><<<nbx2, NT, SM::X, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, j, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
           continue;
         }
         if (mode == 3) {
-          k_x2<L, X2_OBJ><<<nbx2, NT, SM::ROWS, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, j, N);
+          k_x2<L, X2_OBJ><<<nbx2, NT, SM::X, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, j, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8 / 2, N * fl * 2);
           continue;
         }
         if (mode == 0) {
-          k_x2<L, X2_GRAD><<<nbx2, NT, SM::ROWS, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, j, N);
+          k_x2<L, X2_GRAD><<<nbx2, NT, SM::X, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, j, N);
           pend(p, HOLO_PASS_X2, 2 * rN * A + NN8 / 2, N * fl * 4);
         } else {
-          k_x2<L, X2_ADJ><<<nbx2, NT, SM::ROWS, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, j, N);
+          k_x2<L, X2_ADJ><<<nbx2, NT, SM::X, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, j, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
         }
         float2 *Gj = want_q ? p->G + (size_t)j * LL : nullptr;
         float2 *T3j = gpsi ? p->T3 + (size_t)j * LL : nullptr;
         pbeg(p);
-        k_y2<L><<<L / GC, NT, SM::COLS_P, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, tb, k, j, nz, mag, N);
+        k_y2<L><<<L / G, NT, SM::XP, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, tb, k, j, nz, mag, N);
         pend(p, HOLO_PASS_Y2, rN * A + (Gj ? 3 * A : 0) + (T3j ? 2 * A : 0),
              L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0)));
       }
       if (gpsi && (mode == 0 || mode == 2)) {
         pbeg(p);
-        k_x3<L><<<L / GR, NT, SM::ROWS_P, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
+        k_x3<L><<<L / G, NT, SM::XP, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
                                                p->partX3 + (size_t)k * 2 * p->nbx3, tb, k, nz, p->magmask, gscale);
         pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
       }
@@ -428,7 +432,7 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   holo_status s = HOLO_OK;
   const size_t LL = (size_t)L * L;
   auto A = [&](auto **ptr, size_t bytes) { if (s == HOLO_OK) s = dalloc(p, ptr, bytes); };
-  const int GR = 8192 / L;  // rows per CTA of the row kernels (Cta<L, false>::G)
+  const int GR = 16 * NT / L;  // lines per CTA of the line kernels (CtaK<L>::G)
   p->nbx2 = (N + GR - 1) / GR;
   p->nbx3 = L / GR;
   const size_t Kc = (size_t)(K > 0 ? K : 1);
