@@ -14,10 +14,9 @@
 // round trip.  Only the S16 exchanges between stages go through shared memory:
 // 2 per transform for L = 512 ... 4096 (one STS.64 + one LDS.64 per element each).
 //
-// Exchange buffers are double-buffered per group: exchange e writes buffer e&1,
-// which makes ONE __syncthreads() per exchange sufficient (the next write to the
-// same buffer is two exchanges later, behind another barrier that every reader
-// of this one has passed).  Element i sits at padded slot P(i) = i + i/16, so the
+// Exchange buffers: one per line (HOLO_SINGLE_BUF, default; a barrier before each
+// write and one before the reads) or two (exchange e writes buffer e&1, then ONE
+// barrier per exchange suffices).  Element i sits at padded slot P(i) = i + i/16, so the
 // layout-S reads and the radix-16 / radix-F scatters are bank-conflict free for
 // 64-bit accesses within a group.
 //
@@ -33,12 +32,14 @@
 
 // Build knobs (compile-time, for the engine microbenchmark tools/fftbench.cu):
 //   HOLO_TW_FULL   1: load all 15 stage twiddles from a [stage][m][16] table instead of 4 powers
-//   HOLO_SINGLE_BUF 1: one exchange buffer per line, two barriers per exchange
+//   HOLO_SINGLE_BUF 1 (default): one exchange buffer per line, two barriers per exchange;
+//                   0: double-buffered, one barrier per exchange, twice the shared memory
+//                   (measured 4% slower in the full sweep: the freed space serves L1 / table slots)
 #ifndef HOLO_TW_FULL
 #define HOLO_TW_FULL 0
 #endif
 #ifndef HOLO_SINGLE_BUF
-#define HOLO_SINGLE_BUF 0
+#define HOLO_SINGLE_BUF 1
 #endif
 
 namespace holo {

@@ -25,6 +25,7 @@
 // All tables are fp64-generated on the host, phases reduced in cycles.
 #pragma once
 #include "fft_engine.cuh"
+#include "tma.cuh"
 
 namespace holo {
 
@@ -54,7 +55,7 @@ struct Cta {
   // per-group stride (two buffers) skewed so that the groups sharing a 16-lane
   // phase land on distinct banks
   static constexpr int SKEW = G <= 16 ? 16 / G : 1;
-  static constexpr int GS = 2 * LPB + SKEW;
+  static constexpr int GS = (HOLO_SINGLE_BUF ? 1 : 2) * LPB + SKEW;
   static constexpr size_t XBYTES = sizeof(float2) * (size_t)GS * G;
   static constexpr size_t PRIV = sizeof(float2) * 16 * NT;  // one thread-private line
   __device__ __forceinline__ static int g() { return threadIdx.x % G; }
@@ -107,63 +108,176 @@ __device__ __forceinline__ void mul_tab(float2 (&v)[16], const float2 *__restric
   }
 }
 
-// ---- magnification ----------------------------------------------------------------
-struct MagTabs {
-  const float2 *cr, *wodd, *bke, *bko, *cout, *cwo;
+// ---- table pipeline --------------------------------------------------------------
+// The pointwise factors of a launch (chirps, Bluestein kernel spectra, transfer
+// functions: one length-L table per step) are streamed into two shared-memory slots
+// by 1-D bulk copies (cp.async.bulk + mbarrier), each issued one transform ahead of
+// its use: the FFT hides the L2 latency that a direct load would expose.  The
+// launch's table sequence is a kernel parameter (built on the host).
+constexpr int MAXTAB = 40;
+struct TabSeq {
+  const float2 *p[MAXTAB];
+  int n;
 };
-__device__ __forceinline__ MagTabs mag_tabs(const Tables &tb, int L, int j, const float2 *cr) {
-  return MagTabs{cr, tb.wodd, tb.bke + (size_t)j * L, tb.bko + (size_t)j * L, tb.cout + (size_t)j * L,
-                 tb.cwo + (size_t)j * L};
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
 }
 
-// Forward M S along the line: SRC(r) returns the spectrum X at register r (layout S,
-// natural frequency order); v receives the spatial result y.
-template <int L, class Src>
-__device__ __forceinline__ void mag_fwd(float2 (&v)[16], Src src, const MagTabs &m, Xch &x, int t,
-                                        const float4 *__restrict__ tw) {
-  constexpr int T = L / 16;
-  float2 e[16];
-#pragma unroll
-  for (int r = 0; r < 16; r++) v[r ^ 8] = cmul(src(r), ldg2(m.cr + t + r * T));
-  fft<L, false>(v, x, t, tw);
-  mul_tab<L, false>(v, m.bke, t);
-  fft<L, true>(v, x, t, tw);
-#pragma unroll
-  for (int r = 0; r < 16; r++) e[r] = cmul(v[r], ldg2(m.cout + t + r * T));
-#pragma unroll
-  for (int r = 0; r < 16; r++) v[r ^ 8] = cmul(cmul(src(r), ldg2(m.cr + t + r * T)), ldg2(m.wodd + t + (r ^ 8) * T));
-  fft<L, false>(v, x, t, tw);
-  mul_tab<L, false>(v, m.bko, t);
-  fft<L, true>(v, x, t, tw);
-#pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = cadd(e[r], cmul(v[r], ldg2(m.cwo + t + r * T)));
+template <int L>
+struct TabPipe {
+  float2 *slot;   // 2 * L float2 of shared memory
+  uint64_t *bar;  // 2 mbarriers in shared memory
+  int used;       // tables taken so far (uniform over the CTA)
+  static constexpr size_t BYTES = 2 * sizeof(float2) * L;
+
+  __device__ __forceinline__ void issue(const TabSeq &q, int i) {
+    if (threadIdx.x == 0 && i < q.n) {
+      fence_proxy_async();  // earlier generic reads of this slot precede the async write
+      mbar_expect_tx(bar + (i & 1), L * sizeof(float2));
+      bulk_g2s(slot + (i & 1) * L, q.p[i], L * sizeof(float2), bar + (i & 1));
+    }
+  }
+  // all threads; starts tables 0 and 1
+  __device__ __forceinline__ void start(const TabSeq &q, float2 *sm_slots, uint64_t *bars) {
+    slot = sm_slots;
+    bar = bars;
+    used = 0;
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      mbar_init(bar + 1, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    issue(q, 0);
+    issue(q, 1);
+  }
+  // Table i = used: wait for it, then refill the other slot with table i + 1 (its
+  // previous content, table i - 1, was consumed before a transform barrier; pass
+  // sync = true when no transform separates the use of table i - 1 from this call).
+  __device__ __forceinline__ const float2 *take(const TabSeq &q, bool sync = false) {
+    const int i = used++;
+    if (i >= 1) {
+      if (sync) __syncthreads();
+      issue(q, i + 1);
+    }
+    mbar_wait(bar + (i & 1), (i >> 1) & 1);
+    return slot + (i & 1) * L;
+  }
+};
+
+// w[i] = e^{-i pi i / L} at i = t + T q (T = L/16): e^{-i pi t/L} e^{-i pi q/16}
+__device__ __forceinline__ float2 wodd_base(int t, int L) {
+  float s, c;
+  sincospif(-(float)t / (float)L, &s, &c);
+  return make_float2(c, s);
+}
+template <int Q>
+__device__ __forceinline__ float2 wodd_q(float2 base) {
+  // cos / sin (pi Q / 16), Q = 0..15
+  constexpr float C[16] = {1.0f, 0.98078528040323044913f, 0.92387953251128675613f, 0.83146961230254523708f,
+                           0.70710678118654752440f, 0.55557023301960222474f, 0.38268343236508977173f,
+                           0.19509032201612826785f, 0.0f, -0.19509032201612826785f, -0.38268343236508977173f,
+                           -0.55557023301960222474f, -0.70710678118654752440f, -0.83146961230254523708f,
+                           -0.92387953251128675613f, -0.98078528040323044913f};
+  constexpr float S[16] = {0.0f, 0.19509032201612826785f, 0.38268343236508977173f, 0.55557023301960222474f,
+                           0.70710678118654752440f, 0.83146961230254523708f, 0.92387953251128675613f,
+                           0.98078528040323044913f, 1.0f, 0.98078528040323044913f, 0.92387953251128675613f,
+                           0.83146961230254523708f, 0.70710678118654752440f, 0.55557023301960222474f,
+                           0.38268343236508977173f, 0.19509032201612826785f};
+  return cmul(base, make_float2(C[Q], -S[Q]));
 }
 
-// Adjoint (M S)^* along the line: SRC(r) returns the spatial input y at register r;
-// v receives the SPECTRUM W[f] (natural order) of the result; the caller finishes
-// with an inverse FFT (possibly after summing several W).
-template <int L, class Src>
-__device__ __forceinline__ void mag_adj(float2 (&v)[16], Src src, const MagTabs &m, Xch &x, int t,
-                                        const float4 *__restrict__ tw) {
+// ---- magnification ----------------------------------------------------------------
+// Forward M S along the line (reading C1):
+//   a[i] = cr[f] X[f] (i = f + L/2 mod L),  E = IFFT(FFT(a) bke),  O = IFFT(FFT(a w) bko),
+//   y[o] = cout[o] (E[o] + conj(w[o]) O[o]).
+// SRC(r): spectrum X at register r (layout S, natural frequency order).  E is parked
+// with STASH(r, e) between the two transform pairs and fetched back with UNSTASH(r);
+// SRC(r) is read before STASH(r, .) for the same r, so source and stash may share a
+// thread-private slot: only one line is live across each transform.  w is computed on
+// the fly; the pipe supplies, in order: cr, bke, cr, bko, cout.  v receives y.
+template <int L, class Src, class Stash, class Unstash>
+__device__ __forceinline__ void mag_fwd(float2 (&v)[16], Src src, Stash stash, Unstash unstash, TabPipe<L> &pipe,
+                                        const TabSeq &q, bool sync0, Xch &x, int t, const float4 *__restrict__ tw) {
   constexpr int T = L / 16;
-  float2 e[16];
+  const float2 *tab = pipe.take(q, sync0);  // cr
 #pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = cmulc(src(r), ldg2(m.cout + t + r * T));
+  for (int r = 0; r < 16; r++) v[r ^ 8] = cmul(src(r), tab[t + r * T]);
   fft<L, false>(v, x, t, tw);
-  mul_tab<L, true>(v, m.bke, t);
+  tab = pipe.take(q);  // bke
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cmul(v[r], tab[t + r * T]);
   fft<L, true>(v, x, t, tw);
+  tab = pipe.take(q);  // cr again
+  const float2 wb = wodd_base(t, L);
+  float2 s[16];
 #pragma unroll
-  for (int r = 0; r < 16; r++) e[r] = v[r];
-#pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = cmulc(src(r), ldg2(m.cwo + t + r * T));
+  for (int r = 0; r < 16; r++) {
+    s[r] = src(r);
+    stash(r, v[r]);
+  }
+#define HOLO_B(R) v[(R) ^ 8] = cmul(cmul(s[R], tab[t + (R) * T]), wodd_q<(R) ^ 8>(wb));
+  HOLO_B(0) HOLO_B(1) HOLO_B(2) HOLO_B(3) HOLO_B(4) HOLO_B(5) HOLO_B(6) HOLO_B(7)
+  HOLO_B(8) HOLO_B(9) HOLO_B(10) HOLO_B(11) HOLO_B(12) HOLO_B(13) HOLO_B(14) HOLO_B(15)
+#undef HOLO_B
   fft<L, false>(v, x, t, tw);
-  mul_tab<L, true>(v, m.bko, t);
+  tab = pipe.take(q);  // bko
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cmul(v[r], tab[t + r * T]);
   fft<L, true>(v, x, t, tw);
-  // Z[i] = E[i] + conj(w[i]) O[i];  W[f] = conj(cr[f]) Z[(f + L/2) mod L]
+  tab = pipe.take(q);  // cout
+#define HOLO_C(R) v[R] = cmul(cadd(unstash(R), cmulc(v[R], wodd_q<R>(wb))), tab[t + (R) * T]);
+  HOLO_C(0) HOLO_C(1) HOLO_C(2) HOLO_C(3) HOLO_C(4) HOLO_C(5) HOLO_C(6) HOLO_C(7)
+  HOLO_C(8) HOLO_C(9) HOLO_C(10) HOLO_C(11) HOLO_C(12) HOLO_C(13) HOLO_C(14) HOLO_C(15)
+#undef HOLO_C
+}
+
+// Adjoint (M S)^* along the line (the steps of mag_fwd conjugated, in reverse):
+//   A = y conj(cout),  Za = IFFT(FFT(A) conj(bke)),  Zb = IFFT(FFT(A w) conj(bko)),
+//   Z[i] = Za[i] + conj(w[i]) Zb[i],  W[f] = conj(cr[f]) Z[(f + L/2) mod L].
+// SRC(r): spatial input y at register r; STASH / UNSTASH as in mag_fwd.  The pipe
+// supplies, in order: cout, bke, cout, bko, cr.  v receives the SPECTRUM W (natural
+// order); the caller finishes with an inverse FFT (possibly after summing several W).
+template <int L, class Src, class Stash, class Unstash>
+__device__ __forceinline__ void mag_adj(float2 (&v)[16], Src src, Stash stash, Unstash unstash, TabPipe<L> &pipe,
+                                        const TabSeq &q, bool sync0, Xch &x, int t, const float4 *__restrict__ tw) {
+  constexpr int T = L / 16;
+  const float2 *tab = pipe.take(q, sync0);  // cout
 #pragma unroll
-  for (int r = 0; r < 16; r++) e[r] = cadd(e[r], cmulc(v[r], ldg2(m.wodd + t + r * T)));
+  for (int r = 0; r < 16; r++) v[r] = cmulc(src(r), tab[t + r * T]);
+  fft<L, false>(v, x, t, tw);
+  tab = pipe.take(q);  // bke
 #pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = cmulc(e[r ^ 8], ldg2(m.cr + t + r * T));
+  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], tab[t + r * T]);
+  fft<L, true>(v, x, t, tw);
+  tab = pipe.take(q);  // cout again
+  const float2 wb = wodd_base(t, L);
+  float2 s[16];
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    s[r] = src(r);
+    stash(r, v[r]);
+  }
+#define HOLO_B(R) v[R] = cmul(cmulc(s[R], tab[t + (R) * T]), wodd_q<R>(wb));
+  HOLO_B(0) HOLO_B(1) HOLO_B(2) HOLO_B(3) HOLO_B(4) HOLO_B(5) HOLO_B(6) HOLO_B(7)
+  HOLO_B(8) HOLO_B(9) HOLO_B(10) HOLO_B(11) HOLO_B(12) HOLO_B(13) HOLO_B(14) HOLO_B(15)
+#undef HOLO_B
+  fft<L, false>(v, x, t, tw);
+  tab = pipe.take(q);  // bko
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], tab[t + r * T]);
+  fft<L, true>(v, x, t, tw);
+#define HOLO_Z(R) s[R] = cadd(unstash(R), cmulc(v[R], wodd_q<R>(wb)));
+  HOLO_Z(0) HOLO_Z(1) HOLO_Z(2) HOLO_Z(3) HOLO_Z(4) HOLO_Z(5) HOLO_Z(6) HOLO_Z(7)
+  HOLO_Z(8) HOLO_Z(9) HOLO_Z(10) HOLO_Z(11) HOLO_Z(12) HOLO_Z(13) HOLO_Z(14) HOLO_Z(15)
+#undef HOLO_Z
+  tab = pipe.take(q);  // cr
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cmulc(s[r ^ 8], tab[t + r * T]);
 }
 
 // ---- deterministic block reduction --------------------------------------------------

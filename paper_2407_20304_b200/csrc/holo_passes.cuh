@@ -21,6 +21,11 @@ template <int L>
 __device__ __forceinline__ float2 *priv_base(float2 *sm) {
   return sm + CtaK<L>::XBYTES / sizeof(float2);
 }
+// table slots follow the exchange space (and the private line when PRIV)
+template <int L, bool PRIV>
+__device__ __forceinline__ float2 *slot_base(float2 *sm) {
+  return sm + (CtaK<L>::XBYTES + (PRIV ? CtaK<L>::PRIV : 0)) / sizeof(float2);
+}
 
 // layout-S line access of a P2 array with R rows: row y (x = t + T r) / column x (y = t + T r)
 template <int L>
@@ -48,12 +53,16 @@ __device__ __forceinline__ void st_p2_col(const float2 (&v)[16], float2 *__restr
 // rows of psi_k (row-major):  X = FFT(psi row) (kept thread-private); per j: T1_j row = M_{1/mt_j} S_{sx} psi row
 template <int L>
 __global__ void __launch_bounds__(NT, 1)
-    k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1, Tables tb, int k, int nz, uint32_t magmask) {
+    k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1, Tables tb, const __grid_constant__ TabSeq seq,
+         int nz, uint32_t magmask) {
   using C = CtaK<L>;
   extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
   const Priv<NT> X{priv_base<L>(sm)};
+  TabPipe<L> pipe;
+  pipe.start(seq, slot_base<L, true>(sm), bars);
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 v[16];
   ld_row<L>(v, psi_k + (size_t)y * L, t);
@@ -61,12 +70,16 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
   for (int r = 0; r < 16; r++) X[r] = v[r];
   for (int j = 0; j < nz; j++) {
-    const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 0) * L;
     if ((magmask >> j) & 1u) {
-      mag_fwd<L>(v, [&](int r) { return X[r]; }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
+      // X (thread-private smem) is reused by every plane: the first half's term stays in registers
+      float2 e[16];
+      mag_fwd<L>(
+          v, [&](int r) { return X[r]; }, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe,
+          seq, j > 0, x, t, tb.tw);
     } else {
+      const float2 *cr = pipe.take(seq, j > 0);
 #pragma unroll
-      for (int r = 0; r < 16; r++) v[r] = cmul(X[r], ldg2(cr + t + r * (L / 16)));
+      for (int r = 0; r < 16; r++) v[r] = cmul(X[r], cr[t + r * (L / 16)]);
       fft<L, true>(v, x, t, tb.tw);
     }
     st_p2_row<L>(v, T1 + (size_t)j * L * L, y, L, t);
@@ -79,24 +92,30 @@ __global__ void __launch_bounds__(NT, 1)
 template <int L>
 __global__ void __launch_bounds__(NT, 1)
     k_y1(const float2 *__restrict__ T1j, const float2 *__restrict__ qj, float2 *__restrict__ Aout,
-         float2 *__restrict__ W1, Tables tb, int k, int j, int nz, int mag, int N) {
+         float2 *__restrict__ W1, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
   const Priv<NT> X{priv_base<L>(sm)};
+  TabPipe<L> pipe;
+  pipe.start(seq, slot_base<L, true>(sm), bars);
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
-  const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 1) * L;
   float2 v[16];
   ld_p2_col<L>(v, T1j, col, L, t);
   fft<L, false>(v, x, t, tb.tw);
   if (mag) {
 #pragma unroll
     for (int r = 0; r < 16; r++) X[r] = v[r];
-    mag_fwd<L>(v, [&](int r) { return X[r]; }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
+    mag_fwd<L>(
+        v, [&](int r) { return X[r]; }, [&](int r, float2 e) { X[r] = e; }, [&](int r) { return X[r]; }, pipe, seq,
+        false, x, t, tb.tw);
   } else {
-    mul_tab<L, false>(v, cr, t);
+    const float2 *cr = pipe.take(seq);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmul(v[r], cr[t + r * T]);
     fft<L, true>(v, x, t, tb.tw);
   }
   if (Aout) st_p2_col<L>(v, Aout, col, L, t);
@@ -104,7 +123,9 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + p2(t + r * T, col, L)));
     fft<L, false>(v, x, t, tb.tw);
-    mul_tab<L, false>(v, tb.hdet + (size_t)j * L, t);
+    const float2 *h = pipe.take(seq);  // hdet_j / L
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmul(v[r], h[t + r * T]);
     fft<L, true>(v, x, t, tb.tw);
     const int o = (L - N) / 2;
 #pragma unroll
@@ -123,23 +144,27 @@ __global__ void __launch_bounds__(NT, 1)
 template <int L, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_x2(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
-         double *__restrict__ partial, Tables tb, int j, int N) {
+         double *__restrict__ partial, Tables tb, const __grid_constant__ TabSeq seq, int N) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
   __shared__ double red[32];
+  __shared__ uint64_t bars[2];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
+  TabPipe<L> pipe;  // hdet_j / L (GRAD: twice)
+  pipe.start(seq, slot_base<L, false>(sm), bars);
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   const bool act = y < N;
   const int o = (L - N) / 2;
-  const float2 *h = tb.hdet + (size_t)j * L;
   float2 v[16];
   if (MODE != X2_ADJ) {
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = act ? ldg2(in + p2(y, t + r * T, N)) : make_float2(0.f, 0.f);
     fft<L, false>(v, x, t, tb.tw);
-    mul_tab<L, false>(v, h, t);
+    const float2 *h = pipe.take(seq);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmul(v[r], h[t + r * T]);
     fft<L, true>(v, x, t, tb.tw);
     if (MODE == X2_FWD) {
       if (act) {
@@ -177,7 +202,9 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   fft<L, false>(v, x, t, tb.tw);
-  mul_tab<L, true>(v, h, t);
+  const float2 *h = pipe.take(seq);
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], h[t + r * T]);
   fft<L, true>(v, x, t, tb.tw);
   if (act) st_p2_row<L>(v, out, y, N, t);
 }
@@ -187,13 +214,17 @@ __global__ void __launch_bounds__(NT, 1)
 template <int L>
 __global__ void __launch_bounds__(NT, 1)
     k_y2(const float2 *__restrict__ V1, const float2 *__restrict__ a, const float2 *__restrict__ qj,
-         float2 *__restrict__ Gj, float2 *__restrict__ T3j, Tables tb, int k, int j, int nz, int mag, int N) {
+         float2 *__restrict__ Gj, float2 *__restrict__ T3j, Tables tb, const __grid_constant__ TabSeq seq, int mag,
+         int N) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
   const Priv<NT> Y{priv_base<L>(sm)};
+  TabPipe<L> pipe;
+  pipe.start(seq, slot_base<L, true>(sm), bars);
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
   const int o = (L - N) / 2;
   float2 v[16];
@@ -203,7 +234,11 @@ __global__ void __launch_bounds__(NT, 1)
     v[r] = (row >= 0 && row < N) ? ldg2(V1 + p2(row, col, N)) : make_float2(0.f, 0.f);
   }
   fft<L, false>(v, x, t, tb.tw);
-  mul_tab<L, true>(v, tb.hdet + (size_t)j * L, t);
+  {
+    const float2 *h = pipe.take(seq);  // hdet_j / L, conjugated
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], h[t + r * T]);
+  }
   fft<L, true>(v, x, t, tb.tw);
   if (Gj) {
 #pragma unroll
@@ -215,14 +250,17 @@ __global__ void __launch_bounds__(NT, 1)
   if (!T3j) return;
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));
-  const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 1) * L;
   if (mag) {
 #pragma unroll
     for (int r = 0; r < 16; r++) Y[r] = v[r];
-    mag_adj<L>(v, [&](int r) { return Y[r]; }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
+    mag_adj<L>(
+        v, [&](int r) { return Y[r]; }, [&](int r, float2 e) { Y[r] = e; }, [&](int r) { return Y[r]; }, pipe, seq,
+        true, x, t, tb.tw);
   } else {
     fft<L, false>(v, x, t, tb.tw);
-    mul_tab<L, true>(v, cr, t);
+    const float2 *cr = pipe.take(seq);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
   }
   fft<L, true>(v, x, t, tb.tw);
   st_p2_col<L>(v, T3j, col, L, t);
@@ -234,44 +272,44 @@ __global__ void __launch_bounds__(NT, 1)
 template <int L>
 __global__ void __launch_bounds__(NT, 1)
     k_x3(const float2 *__restrict__ T3, const float2 *__restrict__ eta, float2 *__restrict__ g,
-         double *__restrict__ partial, Tables tb, int k, int nz, uint32_t magmask, float scale) {
+         double *__restrict__ partial, Tables tb, const __grid_constant__ TabSeq seq, int nz, uint32_t magmask,
+         float scale) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
   __shared__ double red[32];
+  __shared__ uint64_t bars[2];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
-  const Priv<NT> W{priv_base<L>(sm)};
+  const Priv<NT> Z{priv_base<L>(sm)};
+  TabPipe<L> pipe;
+  pipe.start(seq, slot_base<L, true>(sm), bars);
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  float2 *grow = g + (size_t)y * L;  // also the Fourier-domain accumulator of sum_j W_j
   float2 v[16];
   for (int j = 0; j < nz; j++) {
     const float2 *T3j = T3 + (size_t)j * L * L;
-    const float2 *cr = tb.cr + ((size_t)(k * nz + j) * 2 + 0) * L;
     if ((magmask >> j) & 1u) {
-      mag_adj<L>(v, [&](int r) { return ldg2(T3j + p2(y, t + r * T, L)); }, mag_tabs(tb, L, j, cr), x, t, tb.tw);
+      mag_adj<L>(
+          v, [&](int r) { return ldg2(T3j + p2(y, t + r * T, L)); }, [&](int r, float2 e) { Z[r] = e; },
+          [&](int r) { return Z[r]; }, pipe, seq, j > 0, x, t, tb.tw);
     } else {
       ld_p2_row<L>(v, T3j, y, L, t);
       fft<L, false>(v, x, t, tb.tw);
-      mul_tab<L, true>(v, cr, t);
+      const float2 *cr = pipe.take(seq);
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
     }
-    if (j == 0) {
+    if (j + 1 < nz) {
 #pragma unroll
-      for (int r = 0; r < 16; r++) W[r] = v[r];
-    } else if (j + 1 < nz) {
+      for (int r = 0; r < 16; r++) grow[t + r * T] = j == 0 ? v[r] : cadd(grow[t + r * T], v[r]);
+    } else if (j > 0) {
 #pragma unroll
-      for (int r = 0; r < 16; r++) W[r] = cadd(W[r], v[r]);
-    } else {
-#pragma unroll
-      for (int r = 0; r < 16; r++) v[r] = cadd(W[r], v[r]);
+      for (int r = 0; r < 16; r++) v[r] = cadd(grow[t + r * T], v[r]);
     }
-  }
-  if (nz == 1) {
-#pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = W[r];
   }
   fft<L, true>(v, x, t, tb.tw);
   double gg = 0.0, ge = 0.0;
-  float2 *grow = g + (size_t)y * L;
 #pragma unroll
   for (int r = 0; r < 16; r++) {
     const float2 a = cscale(v[r], scale);

@@ -154,22 +154,23 @@ bool supported_L(int L) { return L == 128 || L == 256 || L == 512 || L == 1024 |
 
 template <int L>
 struct Smem {
-  static constexpr size_t X = CtaK<L>::XBYTES;            // exchange space only
-  static constexpr size_t XP = X + CtaK<L>::PRIV;         // + one thread-private line (Bluestein kernels)
+  static constexpr size_t X = CtaK<L>::XBYTES;                      // exchange space only (filters)
+  static constexpr size_t XT = X + TabPipe<L>::BYTES;                // + two table slots
+  static constexpr size_t XPT = X + CtaK<L>::PRIV + TabPipe<L>::BYTES;  // + one thread-private line
 };
 
 template <int L>
 void set_smem_attrs() {
   using S = Smem<L>;
   auto a = [](const void *f, size_t s) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s); };
-  a((const void *)k_x1<L>, S::XP);
-  a((const void *)k_y1<L>, S::XP);
-  a((const void *)k_x2<L, X2_GRAD>, S::X);
-  a((const void *)k_x2<L, X2_FWD>, S::X);
-  a((const void *)k_x2<L, X2_ADJ>, S::X);
-  a((const void *)k_x2<L, X2_OBJ>, S::X);
-  a((const void *)k_y2<L>, S::XP);
-  a((const void *)k_x3<L>, S::XP);
+  a((const void *)k_x1<L>, S::XPT);
+  a((const void *)k_y1<L>, S::XPT);
+  a((const void *)k_x2<L, X2_GRAD>, S::XT);
+  a((const void *)k_x2<L, X2_FWD>, S::XT);
+  a((const void *)k_x2<L, X2_ADJ>, S::XT);
+  a((const void *)k_x2<L, X2_OBJ>, S::XT);
+  a((const void *)k_y2<L>, S::XPT);
+  a((const void *)k_x3<L>, S::XPT);
   a((const void *)k_rows_filter<L, false, true, false>, S::X);
   a((const void *)k_rows_filter<L, true, false, false>, S::X);
   a((const void *)k_rows_filter<L, true, false, true>, S::X);
@@ -290,12 +291,31 @@ struct Run {
     for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
     qj(p, q);
     if (want_q) cudaMemsetAsync(p->G, 0, sizeof(float2) * LL * nz, p->stream);
+    // table sequences of the pipelined pointwise steps (holo_kernels.cuh, TabPipe)
+    auto crp = [&](int k, int j, int ax) { return p->cr + ((size_t)(k * nz + j) * 2 + ax) * L; };
+    auto add_fwd = [&](TabSeq &q, int k, int j, int ax) {  // mag_fwd: cr, bke, cr, bko, cout
+      const float2 *c = crp(k, j, ax);
+      const float2 *list[5] = {c, p->bke + (size_t)j * L, c, p->bko + (size_t)j * L, p->cout + (size_t)j * L};
+      for (auto *e : list) q.p[q.n++] = e;
+    };
+    auto add_adj = [&](TabSeq &q, int k, int j, int ax) {  // mag_adj: cout, bke, cout, bko, cr
+      const float2 *c = p->cout + (size_t)j * L;
+      const float2 *list[5] = {c, p->bke + (size_t)j * L, c, p->bko + (size_t)j * L, crp(k, j, ax)};
+      for (auto *e : list) q.p[q.n++] = e;
+    };
     for (int k = 0; k < K; k++) {
       const float2 *psik = psi + (size_t)k * LL;
       const bool need_fwd_chain = (mode != 2) || want_q;
       if (need_fwd_chain) {
+        TabSeq q{};
+        for (int j = 0; j < nz; j++) {
+          if ((p->magmask >> j) & 1u)
+            add_fwd(q, k, j, 0);
+          else
+            q.p[q.n++] = crp(k, j, 0);
+        }
         pbeg(p);
-        k_x1<L><<<L / G, NT, SM::XP, p->stream>>>(psik, p->T1, tb, k, nz, p->magmask);
+        k_x1<L><<<L / G, NT, SM::XPT, p->stream>>>(psik, p->T1, tb, q, nz, p->magmask);
         pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * (1 + 4 * nmag + (nz - nmag)));
       }
       for (int j = 0; j < nz; j++) {
@@ -306,41 +326,65 @@ struct Run {
         if (need_fwd_chain) {
           float2 *aout = want_q ? p->Aw : nullptr;
           float2 *w1 = (mode == 2) ? nullptr : p->W1;
+          TabSeq q{};
+          if (mag)
+            add_fwd(q, k, j, 1);
+          else
+            q.p[q.n++] = crp(k, j, 1);
+          if (w1) q.p[q.n++] = p->hdet + (size_t)j * L;
           pbeg(p);
-          k_y1<L><<<L / G, NT, SM::XP, p->stream>>>(T1j, qjj, aout, w1, tb, k, j, nz, mag, N);
+          k_y1<L><<<L / G, NT, SM::XPT, p->stream>>>(T1j, qjj, aout, w1, tb, q, mag, N);
           pend(p, HOLO_PASS_Y1, A + (w1 ? A + rN * A : 0) + (aout ? A : 0),
                L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0)));
         }
         double *pf = p->partF + fr * nbx2;
+        TabSeq qh{};
+        qh.p[qh.n++] = p->hdet + (size_t)j * L;
+        if (mode == 0) qh.p[qh.n++] = p->hdet + (size_t)j * L;
         pbeg(p);
         if (mode == 1) {
-          k_x2<L, X2_FWD><<<nbx2, NT, SM::X, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, j, N);
+          k_x2<L, X2_FWD><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, qh, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
           continue;
         }
         if (mode == 3) {
-          k_x2<L, X2_OBJ><<<nbx2, NT, SM::X, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, j, N);
+          k_x2<L, X2_OBJ><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, qh, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8 / 2, N * fl * 2);
           continue;
         }
         if (mode == 0) {
-          k_x2<L, X2_GRAD><<<nbx2, NT, SM::X, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, j, N);
+          k_x2<L, X2_GRAD><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, qh, N);
           pend(p, HOLO_PASS_X2, 2 * rN * A + NN8 / 2, N * fl * 4);
         } else {
-          k_x2<L, X2_ADJ><<<nbx2, NT, SM::X, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, j, N);
+          k_x2<L, X2_ADJ><<<nbx2, NT, SM::XT, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, qh, N);
           pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
         }
         float2 *Gj = want_q ? p->G + (size_t)j * LL : nullptr;
         float2 *T3j = gpsi ? p->T3 + (size_t)j * LL : nullptr;
+        TabSeq q2{};
+        q2.p[q2.n++] = p->hdet + (size_t)j * L;
+        if (T3j) {
+          if (mag)
+            add_adj(q2, k, j, 1);
+          else
+            q2.p[q2.n++] = crp(k, j, 1);
+        }
         pbeg(p);
-        k_y2<L><<<L / G, NT, SM::XP, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, tb, k, j, nz, mag, N);
+        k_y2<L><<<L / G, NT, SM::XPT, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, tb, q2, mag, N);
         pend(p, HOLO_PASS_Y2, rN * A + (Gj ? 3 * A : 0) + (T3j ? 2 * A : 0),
              L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0)));
       }
       if (gpsi && (mode == 0 || mode == 2)) {
+        TabSeq q3{};
+        for (int j = 0; j < nz; j++) {
+          if ((p->magmask >> j) & 1u)
+            add_adj(q3, k, j, 0);
+          else
+            q3.p[q3.n++] = crp(k, j, 0);
+        }
         pbeg(p);
-        k_x3<L><<<L / G, NT, SM::XP, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
-                                               p->partX3 + (size_t)k * 2 * p->nbx3, tb, k, nz, p->magmask, gscale);
+        k_x3<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
+                                                p->partX3 + (size_t)k * 2 * p->nbx3, tb, q3, nz, p->magmask, gscale);
         pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
       }
     }

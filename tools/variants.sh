@@ -1,7 +1,7 @@
 # time tuning-variant builds of libholo (HOLO_LIB) on a short cfg3 bench; parity of each on cfg0/cfg1
 mkdir -p gpurun_out
 ANG=${ANG:-16}
-for lib in paper_2407_20304_b200/libholo.so build_variants/*.so; do
+for lib in paper_2407_20304_b200/libholo.so ${VARIANTS:-build_variants/*.so}; do
   echo "== $lib"
   HOLO_LIB=$lib timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "cfg0 or cfg1 or torus" 2>&1 | tail -1
   HOLO_LIB=$lib timeout 600 python bench.py --angles $ANG --steps 2 --warmup 2 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
