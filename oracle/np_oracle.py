@@ -157,3 +157,23 @@ class Problem:
                 qjs[j] = self.qj(q, j)
             out[(k, j)] = self.frame_fwd(psi[k], qjs[j], j, shifts[k, j])[0]
         return out
+
+
+def grad_ref(wavelength, p0, zeta0, q, ref_shifts, sqrt_dref, want_q=True):
+    """O14 (reference constraint P:102; Eq. (10) reference term P:115; Eq. (12)),
+    numpy.fft as the DFT:  w_r = C(P_{zeta0} S_{s_r} q),  F = sum_r || |w_r| - sqrt_dref_r ||^2,
+    grad_q = 2 sum_r S_{-s_r} P_{-zeta0} Z rho_r,  rho = w - a w/|w| (0 at w = 0)."""
+    L = q.shape[-1]
+    N = sqrt_dref.shape[-1]
+    F = 0.0
+    gq = np.zeros((L, L), np.complex128) if want_q else None
+    for r in range(sqrt_dref.shape[0]):
+        sx, sy = float(ref_shifts[r][0]), float(ref_shifts[r][1])
+        w = crop(prop(shift(q, sx, sy), wavelength, p0, zeta0), N)
+        a = np.asarray(sqrt_dref[r], np.float64)
+        m = np.abs(w)
+        F += float(np.sum((m - a) ** 2))
+        if want_q:
+            rho = np.where(m > 0, w - a * w / np.where(m > 0, m, 1.0), 0.0)
+            gq += 2.0 * shift(prop(zpad(rho, L), wavelength, p0, -zeta0), -sx, -sy)
+    return F, gq

@@ -11,6 +11,7 @@
 
 #include "../../include/holo.h"
 #include "holo_passes.cuh"
+#include "holo_ref.cuh"
 
 using namespace holo;
 using cd = std::complex<double>;
@@ -48,6 +49,10 @@ struct holo_plan {
   uint64_t launches = 0;
   int n_ref = 0;
   std::vector<double> ref_shifts;
+  // reference arm (holo_ref.cuh): Qhat, Ghat (P2, L x L), Wr, Vr (P2, N x L), Href [R][2][L], F partials
+  float2 *Qhat = nullptr, *Ghat = nullptr, *Wr = nullptr, *Vr = nullptr, *Href = nullptr, *tw3 = nullptr;
+  double *partR = nullptr;
+  int ref_cap = 0;  // frames Href / partR are sized for
   // per-pass event profiling (holo_profile_*)
   struct Rec { int id; double bytes, flops; size_t ev; };
   bool prof_on = false;
@@ -150,7 +155,12 @@ std::vector<cd> transfer(int L, double lam, double p0, double z) {
   return h;
 }
 
-bool supported_L(int L) { return L == 128 || L == 256 || L == 512 || L == 1024 || L == 2048 || L == 4096; }
+bool supported_L(int L) {
+  return L == 128 || L == 256 || L == 512 || L == 1024 || L == 2048 || L == 4096 || L == 6144;
+}
+// the object chain (holo_fwd / holo_adj / holo_grad) needs a power-of-two torus; N_p = 6144
+// (configs[4], reading C16) serves reference-arm-only plans (n_angles = 0)
+bool chain_L(int L) { return (L & (L - 1)) == 0; }
 
 template <int L>
 struct Smem {
@@ -177,7 +187,29 @@ void set_smem_attrs() {
   a((const void *)k_cols_filter<L>, S::X);
 }
 
+template <int L>
+void set_ref_attrs() {
+  const int sz = (int)LineEng<L>::SMEM;
+  auto a = [&](const void *f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sz); };
+  a((const void *)k_ref_cols<L, REF_QHAT>);
+  a((const void *)k_ref_cols<L, REF_R1>);
+  a((const void *)k_ref_cols<L, REF_R3>);
+  a((const void *)k_ref_cols<L, REF_FINAL>);
+  a((const void *)k_ref_rows<L, REF_QHAT>);
+  a((const void *)k_ref_rows<L, REF_R2>);
+  a((const void *)k_ref_rows<L, REF_FINAL>);
+}
+
 void set_attrs(int L) {
+  switch (L) {
+    case 128: set_ref_attrs<128>(); break;
+    case 256: set_ref_attrs<256>(); break;
+    case 512: set_ref_attrs<512>(); break;
+    case 1024: set_ref_attrs<1024>(); break;
+    case 2048: set_ref_attrs<2048>(); break;
+    case 4096: set_ref_attrs<4096>(); break;
+    case 6144: set_ref_attrs<6144>(); return;
+  }
   switch (L) {
     case 128: set_smem_attrs<128>(); break;
     case 256: set_smem_attrs<256>(); break;
@@ -426,6 +458,45 @@ holo_status upload_cr(holo_plan *p, const double *s) {
   return HOLO_OK;
 }
 
+// ------------------------------------------------------------------ reference arm runner (O14)
+template <int L>
+struct RefRun {
+  using E = LineEng<L>;
+  static void run(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc) {
+    const int N = p->N, R = p->n_ref;
+    const size_t SM = E::SMEM;
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const float2 *tw3 = p->tw3;
+    const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
+    const double A = 8.0 * L * L, fl = fftf(L);
+    // Qhat = DFT2(q)
+    pbeg(p);
+    k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, tw3, N, 1.f, 0);
+    k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, tw3, N, 0);
+    pend(p, HOLO_PASS_REF, 4 * A, 2.0 * L * fl);
+    for (int r = 0; r < R; r++) {
+      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
+      pbeg(p);
+      k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, tw3, N, 0);
+      k_ref_rows<L, REF_R2><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r * N * N, p->Vr,
+                                                            p->partR + (size_t)r * gn, Hx, tw, tw3, N, 1.f, 0);
+      if (gq) k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, tw3, N, r == 0);
+      pend(p, HOLO_PASS_REF, A * (1.0 + 0.5 + 0.5 + 1.0 / 8 + 0.5 + (gq ? 0.5 + (r ? 2.0 : 1.0) : 0.0)),
+           fl * (L + 2.0 * N + (gq ? L : 0)));
+    }
+    if (gq) {
+      pbeg(p);
+      k_ref_cols<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, p->Ghat, nullptr, tw, tw3, N, 0);
+      k_ref_rows<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, nullptr, gq, nullptr, nullptr, tw, tw3, N,
+                                                               2.0f, acc ? 1 : 0);
+      pend(p, HOLO_PASS_REF, (acc ? 5 : 4) * A, 2.0 * L * fl);
+    }
+    pbeg(p);
+    k_reduce<<<1, 1024, 0, p->stream>>>(p->partR, (size_t)R * gn, 1, sc, 0);
+    pend(p, HOLO_PASS_REDUCE, 8.0 * R * gn, 0);
+  }
+};
+
 holo_status precheck(holo_plan *p) {
   if (!p) return HOLO_EINVAL;
   if (p->sticky) return fail(p, HOLO_ESTATE, "plan is in an error state: " + p->err);
@@ -452,8 +523,8 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
     if (!(g->z1[j] > 0) || !(g->z1[j] < g->focus_to_detector)) return HOLO_EINVAL;
     if (j > 0 && !(g->z1[j] > g->z1[j - 1])) return HOLO_EINVAL;
   }
-  if (L < 16 || (L & (L - 1))) return HOLO_EUNSUPPORTED;
   if (!supported_L(L)) return HOLO_EUNSUPPORTED;
+  if (!chain_L(L) && K > 0) return HOLO_EUNSUPPORTED;
   if (N % 4) return HOLO_EUNSUPPORTED;  // float4 row I/O of N-wide frames
   holo_plan *p = new holo_plan();
   p->device = device;
@@ -480,7 +551,8 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   p->nbx2 = (N + GR - 1) / GR;
   p->nbx3 = L / GR;
   const size_t Kc = (size_t)(K > 0 ? K : 1);
-  const int S16 = radix16_stages(L), F = L >> (4 * S16);
+  const int LT = chain_L(L) ? L : L / 3;  // line length of the Stockham engine (6144 = 3 x 2048)
+  const int S16 = radix16_stages(LT), F = LT >> (4 * S16);
   const size_t twrows = (size_t)F * (((size_t)1 << (4 * S16)) - 1) / 15;  // F (16^S16 - 1) / 15
   A(&p->tw, sizeof(float2) * 4 * twrows);
   A(&p->hdet, sizeof(float2) * L * nz);
@@ -491,13 +563,14 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   A(&p->bko, sizeof(float2) * L * nz);
   A(&p->wodd, sizeof(float2) * L);
   A(&p->cr, sizeof(float2) * L * 2 * nz * Kc);
-  A(&p->T1, sizeof(float2) * LL * nz);
-  A(&p->Aw, sizeof(float2) * LL);
-  A(&p->W1, sizeof(float2) * (size_t)N * L);
-  A(&p->V1, sizeof(float2) * (size_t)N * L);
-  A(&p->T3, sizeof(float2) * LL * nz);
-  A(&p->G, sizeof(float2) * LL * nz);
-  A(&p->QJ, sizeof(float2) * LL * nz);
+  const size_t LLc = K > 0 ? LL : 0;  // object-chain workspace only when the plan holds angles
+  A(&p->T1, sizeof(float2) * LLc * nz);
+  A(&p->Aw, sizeof(float2) * LLc);
+  A(&p->W1, sizeof(float2) * (K > 0 ? (size_t)N * L : 0));
+  A(&p->V1, sizeof(float2) * (K > 0 ? (size_t)N * L : 0));
+  A(&p->T3, sizeof(float2) * LLc * nz);
+  A(&p->G, sizeof(float2) * LLc * nz);
+  A(&p->QJ, sizeof(float2) * LLc * nz);
   A(&p->partF, sizeof(double) * Kc * nz * p->nbx2);
   A(&p->partX3, sizeof(double) * Kc * 2 * p->nbx3);
   A(&p->partQ, sizeof(double) * 2 * 1184);
@@ -507,7 +580,7 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
     // FFT stage twiddle rows: radix-16 stage with Ns = F 16^st holds, per m < Ns,
     // (w^m, w^2m, w^4m, w^8m), w = exp(-2 pi i / (16 Ns))   (fft_engine.cuh)
     std::vector<cd> tw;
-    for (int Ns = F; Ns < L; Ns *= 16)
+    for (int Ns = F; Ns < LT; Ns *= 16)
       for (int m = 0; m < Ns; m++)
         for (int e : {1, 2, 4, 8}) tw.push_back(expi2pi_frac(-(double)((long)m * e) / (16.0 * Ns)));
     if (tw.size() != 4 * twrows) { holo_plan_destroy(p); return HOLO_EUNSUPPORTED; }
@@ -516,7 +589,14 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
     for (int i = 0; i < L; i++) wo[i] = expi2pi_frac(-(double)i / (2.0 * L));  // w[i] = e^{-i pi i / L}
     std::vector<cd> hd, ho, co, cw, be, bo;
     p->cin_host.clear();
-    for (int j = 0; j < nz; j++) {
+    if (!chain_L(L)) {  // radix-3 combine twiddles W_6144^{g k}, g = 1, 2 (holo_ref.cuh)
+      std::vector<cd> t3;
+      for (int g3 = 1; g3 <= 2; g3++)
+        for (int k = 0; k < L / 3; k++) t3.push_back(expi2pi_frac(-(double)(g3 * k) / (double)L));
+      if (s == HOLO_OK) s = dalloc(p, &p->tw3, sizeof(float2) * t3.size());
+      if (s == HOLO_OK) s = upload(p, p->tw3, t3);
+    }
+    for (int j = 0; j < nz && chain_L(L); j++) {
       auto h1 = transfer(L, g->wavelength, p->p0, p->zdet[j]);
       for (auto &h : h1) h /= (double)L;  // the 1/L of the inverse DFT folded in
       auto h2 = transfer(L, g->wavelength, p->p0, p->omega[j]);
@@ -550,12 +630,14 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
         bo.push_back(b[2 * kk + 1] / (2.0 * L));
       }
     }
-    if (s == HOLO_OK) s = upload(p, p->hdet, hd);
-    if (s == HOLO_OK) s = upload(p, p->homega, ho);
-    if (s == HOLO_OK) s = upload(p, p->cout, co);
-    if (s == HOLO_OK) s = upload(p, p->cwo, cw);
-    if (s == HOLO_OK) s = upload(p, p->bke, be);
-    if (s == HOLO_OK) s = upload(p, p->bko, bo);
+    if (chain_L(L)) {
+      if (s == HOLO_OK) s = upload(p, p->hdet, hd);
+      if (s == HOLO_OK) s = upload(p, p->homega, ho);
+      if (s == HOLO_OK) s = upload(p, p->cout, co);
+      if (s == HOLO_OK) s = upload(p, p->cwo, cw);
+      if (s == HOLO_OK) s = upload(p, p->bke, be);
+      if (s == HOLO_OK) s = upload(p, p->bko, bo);
+    }
     if (s == HOLO_OK) s = upload(p, p->wodd, wo);
   }
   if (s == HOLO_OK && K > 0) {  // zero shifts until holo_set_shifts
@@ -632,6 +714,35 @@ holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
   if (n_ref < 0 || (n_ref > 0 && !s)) return fail(p, HOLO_EINVAL, "bad reference shifts");
   for (int i = 0; i < 2 * n_ref; i++)
     if (!std::isfinite(s[i]) || std::fabs(s[i]) >= p->L / 2) return fail(p, HOLO_EINVAL, "shift not finite or >= npad/2");
+  const int L = p->L, N = p->N;
+  const size_t LL = (size_t)L * L;
+  // workspace of the reference arm, allocated on first use
+  if (!p->Qhat) {
+    st = dalloc(p, &p->Qhat, sizeof(float2) * LL);
+    if (st == HOLO_OK) st = dalloc(p, &p->Ghat, sizeof(float2) * LL);
+    if (st == HOLO_OK) st = dalloc(p, &p->Wr, sizeof(float2) * (size_t)N * L);
+    if (st == HOLO_OK) st = dalloc(p, &p->Vr, sizeof(float2) * (size_t)N * L);
+    if (st != HOLO_OK) return st;
+  }
+  if (n_ref > p->ref_cap) {
+    const int nbr = (N + 15) / 1;  // >= R2 CTAs per frame for every engine (G >= 1)
+    st = dalloc(p, &p->Href, sizeof(float2) * 2 * L * (size_t)n_ref);
+    if (st == HOLO_OK) st = dalloc(p, &p->partR, sizeof(double) * (size_t)nbr * n_ref);
+    if (st != HOLO_OK) return st;
+    p->ref_cap = n_ref;
+  }
+  // H[r][ax][f] = h_{zeta0}[f] r_{s_ax}[f] / L  (O3 x O4 per axis; ax 0: x, 1: y)
+  const auto h = transfer(L, p->g.wavelength, p->p0, p->zeta[0]);
+  std::vector<float2> H((size_t)2 * L * n_ref);
+  for (int r = 0; r < n_ref; r++)
+    for (int ax = 0; ax < 2; ax++) {
+      const double sv = s[2 * r + ax];
+      for (int f = 0; f < L; f++) {
+        const cd v = h[f] * expi2pi_frac(-(double)fbar(f, L) * sv / (double)L) / (double)L;
+        H[((size_t)r * 2 + ax) * L + f] = make_float2((float)v.real(), (float)v.imag());
+      }
+    }
+  if (n_ref > 0) HC(cudaMemcpy(p->Href, H.data(), H.size() * sizeof(float2), cudaMemcpyHostToDevice));
   p->n_ref = n_ref;
   p->ref_shifts.assign(s, s + 2 * n_ref);
   return HOLO_OK;
@@ -685,8 +796,24 @@ holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref, v
                           uint32_t flags) {
   holo_status st = precheck(p);
   if (st != HOLO_OK) return st;
-  (void)q; (void)sqrt_dref; (void)grad_q_part; (void)sc; (void)flags;
-  return fail(p, HOLO_EUNSUPPORTED, "holo_grad_ref: reference arm not built yet");
+  if (!q || !sc || (p->n_ref > 0 && !sqrt_dref)) return fail(p, HOLO_EINVAL, "null pointer");
+  HC(cudaMemsetAsync(sc, 0, sizeof(double), p->stream));
+  const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0, acc = (flags & HOLO_ACCUMULATE_Q) != 0;
+  float2 *gq = obj ? nullptr : (float2 *)grad_q_part;
+  if (p->n_ref == 0) {
+    if (gq && !acc) HC(cudaMemsetAsync(gq, 0, sizeof(float2) * (size_t)p->L * p->L, p->stream));
+    return HOLO_OK;
+  }
+  switch (p->L) {
+    case 128: RefRun<128>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
+    case 256: RefRun<256>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
+    case 512: RefRun<512>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
+    case 1024: RefRun<1024>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
+    case 2048: RefRun<2048>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
+    case 4096: RefRun<4096>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
+    case 6144: RefRun<6144>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
+  }
+  return postcheck(p);
 }
 
 holo_status holo_q_dots(holo_plan *p, const void *grad_q, const void *eta_q_prev, double *out) {

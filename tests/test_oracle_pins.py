@@ -416,3 +416,19 @@ def test_o13_truth_is_a_fixed_point():
     x, hist = ocg.run(sweep, [psi_t, q_t], [1.0, 1.0], 2, max_halvings=3)
     assert all(h["F"] < 1e-20 for h in hist)
     assert rel(x[0], psi_t) < 1e-10 and rel(x[1], q_t) < 1e-10
+
+
+def test_o14_numpy_reference_arm_equals_c_oracle():
+    """np_oracle.grad_ref (numpy.fft DFT) against the naive-DFT C oracle's O14 (R = 3, ragged shifts)."""
+    from oracle import np_oracle as npo
+    cfg = synth.CONFIGS["cfg4"]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    L, N, R = 32, 16, 3
+    rng = np.random.default_rng(14)
+    q = 1 + 0.2 * (rng.standard_normal((L, L)) + 1j * rng.standard_normal((L, L)))
+    rs = rng.uniform(-5, 5, size=(R, 2))
+    d = np.abs(rng.standard_normal((R, N, N)))
+    Fc, gc = oracle.grad_ref(g, q, rs, d)
+    Fn, gn = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs, d)
+    assert abs(Fn - Fc) / Fc < 1e-12
+    assert rel(gn, gc) < 1e-11
