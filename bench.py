@@ -139,6 +139,8 @@ def run_reference(args):
     import oracle
     from oracle import np_oracle as npo
     g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    if cfg.name == "cfg4":
+        return run_reference_ref_arm(args, cfg, g, npo)
     pr = npo.Problem(g, cfg.npad, cfg.n)
     K = 2
     psi_t = synth.psi_stack(cfg, K=K).numpy()
@@ -174,6 +176,84 @@ def run_reference(args):
                       "vs_baseline": None}))
 
 
+def setup_reference_arm(args, world, rank, local, dev, hb, JointCG):
+    """configs[4]: probe-only retrieval from R = 64 x 4 reference frames (psi = 1, reading C16),
+    q-only CG (rho_psi unused, no angles); frames sharded over ranks, grad_q allreduced."""
+    cfg = synth.CONFIGS["cfg4"]
+    R_total = cfg.n_angles
+    R = R_total // world
+    r0 = rank * R
+    plan = hb.Plan(cfg.n, cfg.npad, cfg.z1, 0, cfg.wavelength, cfg.Z, cfg.det_pixel, device=local)
+    plan.set_ref_shifts(synth.ref_shifts(cfg)[r0:r0 + R])
+    q_t = synth.probe(cfg, device=dev, dtype=torch.complex64)
+    w = torch.empty(R, cfg.n, cfg.n, dtype=torch.complex64, device=dev)
+    plan.fwd_ref(q_t, w)
+    inten = w.abs().square_()
+    del w
+    sqrt_dref = synth.poisson_amplitude(inten, cfg.photons, cfg, item=rank).float().contiguous()
+    del inten
+    torch.cuda.empty_cache()
+    rho_q = args.rho_q if args.rho_q is not None else 1.0 / R_total
+    q0 = (q_t * torch.exp(0.2j * torch.linspace(-1, 1, cfg.npad, device=dev))[None, :]).contiguous()
+    solver = JointCG(plan, torch.zeros(0, device=dev), torch.ones(0, cfg.npad, cfg.npad, dtype=torch.complex64,
+                                                                  device=dev), q0, rho_psi=0.0, rho_q=rho_q,
+                     sqrt_dref=sqrt_dref)
+    conf = {"workload": f"cfg4: probe-only, {R_total} reference frames of {cfg.n}^2 on a {cfg.npad}^2 torus "
+                        f"(64 shifts x 4 distances), {R} per GPU", "frames_per_gpu": R, "frames_total": R_total,
+            "n": cfg.n, "npad": cfg.npad, "rho_q": rho_q, "parallelism": f"frame-sharded dp{world}",
+            "l2": "inputs > L2 (each step streams >= 10 GB per GPU; no flush needed)"}
+    return plan, solver, R_total, conf, sqrt_dref, "strong", cfg
+
+
+def cpu_baseline_ref(cfg):
+    """The numpy fp64 O14 oracle on ONE reference frame of configs[4] (6144^2 torus)."""
+    import oracle
+    from oracle import np_oracle as npo
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 0) for t in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    q = synth.probe(cfg).numpy()
+    rs = synth.ref_shifts(cfg)[:1]
+    d = np.ones((1, cfg.n, cfg.n))
+    t0 = time.perf_counter()
+    npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs, d)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"1 reference frame of cfg4: F_ref + grad_q term on the {cfg.npad}^2 torus, numpy fp64 "
+                      f"oracle (oracle/np_oracle.grad_ref); {dt:.2f} s"}
+
+
+def run_reference_ref_arm(args, cfg, g, npo):
+    """--impl reference for configs[4]: the numpy fp64 O14 oracle, one reference frame per step."""
+    q = synth.probe(cfg).numpy()
+    rs = synth.ref_shifts(cfg)
+    d = np.ones((1, cfg.n, cfg.n))
+    for i in range(args.warmup):
+        npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs[i:i + 1], d)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs[i:i + 1], d)
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([t.get("num_threads", 0) for t in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    sample = f"{args.steps} reference frames (one per step) of cfg4: F_ref + grad_q term, numpy fp64 oracle"
+    print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                      "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+                      "impl": "reference", "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": cfg.name, "n": cfg.n, "npad": cfg.npad},
+                      "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                                       "sample": sample},
+                      "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                      "vs_baseline": None}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -198,27 +278,38 @@ def main():
     import paper_2407_20304_b200 as hb
     from paper_2407_20304_b200.solver import JointCG
 
-    cfg, K, k0, scaling = workload(args.workload, world, rank, args.angles)
     dev = torch.device("cuda", local)
-    plan = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=local)
-    plan.set_shifts(synth.shifts(cfg)[k0:k0 + K] if k0 + K <= cfg.n_angles else
-                    np.resize(synth.shifts(cfg), (k0 + K, cfg.nz, 2))[k0:k0 + K])
-    # ---- synthetic measurement: |forward(truth)|^2 with Poisson noise (bench input, not a parity value)
-    q_t = synth.probe(cfg, device=dev, dtype=torch.complex64)
-    psi_t = synth.psi_stack(cfg, K=K, device=dev, dtype=torch.complex64, k0=k0)
-    w = torch.empty(K, cfg.nz, cfg.n, cfg.n, dtype=torch.complex64, device=dev)
-    plan.fwd(psi_t, q_t, w)
-    del psi_t
-    inten = w.abs().square_()
-    del w
-    sqrt_d = synth.poisson_amplitude(inten, cfg.photons, cfg, item=rank).float().contiguous()
-    del inten
-    torch.cuda.empty_cache()
-    K_total = K * world
-    rho_q = args.rho_q if args.rho_q is not None else 1.0 / (K_total)
-    solver = JointCG(plan, sqrt_d, torch.ones(K, cfg.npad, cfg.npad, dtype=torch.complex64, device=dev),
-                     (0.9 * q_t).contiguous(), rho_psi=1.0, rho_q=rho_q)
-    del q_t
+    if args.workload == "cfg4":
+        plan, solver, frames, conf, sqrt_d, scaling, cfg = setup_reference_arm(args, world, rank, local, dev, hb,
+                                                                              JointCG)
+        K_total = 0
+    else:
+        cfg, K, k0, scaling = workload(args.workload, world, rank, args.angles)
+        plan = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=local)
+        plan.set_shifts(synth.shifts(cfg)[k0:k0 + K] if k0 + K <= cfg.n_angles else
+                        np.resize(synth.shifts(cfg), (k0 + K, cfg.nz, 2))[k0:k0 + K])
+        # ---- synthetic measurement: |forward(truth)|^2 with Poisson noise (bench input, not a parity value)
+        q_t = synth.probe(cfg, device=dev, dtype=torch.complex64)
+        psi_t = synth.psi_stack(cfg, K=K, device=dev, dtype=torch.complex64, k0=k0)
+        w = torch.empty(K, cfg.nz, cfg.n, cfg.n, dtype=torch.complex64, device=dev)
+        plan.fwd(psi_t, q_t, w)
+        del psi_t
+        inten = w.abs().square_()
+        del w
+        sqrt_d = synth.poisson_amplitude(inten, cfg.photons, cfg, item=rank).float().contiguous()
+        del inten
+        torch.cuda.empty_cache()
+        K_total = K * world
+        rho_q = args.rho_q if args.rho_q is not None else 1.0 / (K_total)
+        solver = JointCG(plan, sqrt_d, torch.ones(K, cfg.npad, cfg.npad, dtype=torch.complex64, device=dev),
+                         (0.9 * q_t).contiguous(), rho_psi=1.0, rho_q=rho_q)
+        del q_t
+        frames = K_total * cfg.nz
+        conf = {"workload": f"{cfg.name}: {cfg.n}^2 projections on a {cfg.npad}^2 torus, {cfg.nz} distances, "
+                            f"{K} angles per GPU ({K_total} total)",
+                "angles_per_gpu": K, "angles_total": K_total, "distances": cfg.nz, "n": cfg.n,
+                "npad": cfg.npad, "rho_q": rho_q, "parallelism": f"angle-sharded dp{world}",
+                "l2": "inputs > L2 (each step streams >= 25 GB per GPU; no flush needed)"}
     solver.start()
     for _ in range(args.warmup):
         solver.iterate()
@@ -249,7 +340,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    value = K_total * cfg.nz * args.steps / (ms / 1e3)
+    value = frames * args.steps / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (CUDA events on the plan's stream, same region)
     bw, sm_mhz_max, src = peaks()
@@ -305,25 +396,21 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_sweeps = solver.sweeps - sw1
-        e2e = {"value": K_total * cfg.nz * ns / (float(te.item()) / 1e3), "unit": UNIT,
+        e2e = {"value": frames * ns / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(sqrt_d.numel() * 4), "d2h_bytes_per_step": int(40 * e_sweeps / ns),
                "steps": ns}
         del host_d
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg)
+        cpu = cpu_baseline_ref(cfg) if cfg.name == "cfg4" else cpu_baseline(cfg)
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "c64 (fp32 complex; fp64 reductions)", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.n}^2 projections on a {cfg.npad}^2 torus, {cfg.nz} distances, "
-                                   f"{K} angles per GPU ({K_total} total)",
-                       "angles_per_gpu": K, "angles_total": K_total, "distances": cfg.nz, "n": cfg.n,
-                       "npad": cfg.npad, "rho_q": rho_q, "parallelism": f"angle-sharded dp{world}",
-                       "l2": "inputs > L2 (each step streams >= 25 GB per GPU; no flush needed)"},
+            "config": conf,
             "sweeps_per_step": sweeps / args.steps,
             "F_last": hist[-1]["F"], "gamma_last": hist[-1]["gamma"],
             "hbm_frac_step": (tot_bytes / (ms / 1e3) / 1e9) / bw,

@@ -122,6 +122,10 @@ holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float 
 holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref /*[R][n][n]*/,
                           void *grad_q_part, double *sc, uint32_t flags);
 
+/* Reference-arm forward (O14): w[r] = C( P_{zeta0} S_{s_r} q ), complex64 [R][n][n] row-major
+ * (R = n_ref of holo_set_ref_shifts).  Used to synthesise reference frames.            */
+holo_status holo_fwd_ref(holo_plan *p, const void *q, void *w);
+
 /* q-block dot products (run identically on every rank after the allreduce):
  *   out[0] = ||grad_q||^2,  out[1] = Re<grad_q, eta_q_prev> (0 if eta_q_prev NULL).       */
 holo_status holo_q_dots(holo_plan *p, const void *grad_q, const void *eta_q_prev, double *out /*[2] device*/);

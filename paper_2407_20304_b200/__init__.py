@@ -73,6 +73,8 @@ _lib.holo_grad.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_uint32]
 _lib.holo_grad.restype = _S
 _lib.holo_grad_ref.argtypes = [_P, _P, _P, _P, _P, ctypes.c_uint32]
 _lib.holo_grad_ref.restype = _S
+_lib.holo_fwd_ref.argtypes = [_P, _P, _P]
+_lib.holo_fwd_ref.restype = _S
 _lib.holo_q_dots.argtypes = [_P, _P, _P, _P]
 _lib.holo_q_dots.restype = _S
 _lib.holo_cg_step.argtypes = [_P, ctypes.POINTER(HoloCgIn), ctypes.POINTER(HoloCgOut)] + [_P] * 8
@@ -90,7 +92,7 @@ PASS_KERNELS = ["k_x1", "k_y1", "k_x2", "k_y2", "k_x3", "k_rows_filter|k_cols_fi
 
 EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes", "holo_last_error",
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
-            "holo_grad_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
+            "holo_grad_ref", "holo_fwd_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
             "holo_profile_read"]
 
 
@@ -217,6 +219,12 @@ class Plan:
                                      _ptr(sqrt_dref, torch.float32, None, "sqrt_dref"),
                                      _ptr(grad_q_part, torch.complex64, self.npad ** 2, "grad_q_part"),
                                      _ptr(sc, torch.float64, 1, "sc"), flags))
+
+    def fwd_ref(self, q, w):
+        """holo_fwd_ref: w[r] = C(P_{zeta0} S_{s_r} q) for the n_ref reference frames."""
+        self._chk(_lib.holo_fwd_ref(self._h, _ptr(q, torch.complex64, self.npad ** 2, "q"),
+                                    _ptr(w, torch.complex64, None, "w")))
+        return w
 
     def q_dots(self, grad_q, eta_q_prev, out):
         LL = self.npad ** 2

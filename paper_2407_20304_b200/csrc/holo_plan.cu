@@ -198,6 +198,7 @@ void set_ref_attrs() {
   a((const void *)k_ref_rows<L, REF_QHAT>);
   a((const void *)k_ref_rows<L, REF_R2>);
   a((const void *)k_ref_rows<L, REF_FINAL>);
+  a((const void *)k_ref_rows<L, REF_FWD>);
 }
 
 void set_attrs(int L) {
@@ -462,6 +463,27 @@ holo_status upload_cr(holo_plan *p, const double *s) {
 template <int L>
 struct RefRun {
   using E = LineEng<L>;
+  // w[r] = C(P_{zeta0} S_{s_r} q), row-major [R][N][N]
+  static void fwd(holo_plan *p, const float2 *q, float2 *w) {
+    const int N = p->N, R = p->n_ref;
+    const size_t SM = E::SMEM;
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
+    const double A = 8.0 * L * L, fl = fftf(L);
+    pbeg(p);
+    k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, p->tw3, N, 1.f, 0);
+    k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, p->tw3, N, 0);
+    pend(p, HOLO_PASS_REF, 4 * A, 2.0 * L * fl);
+    for (int r = 0; r < R; r++) {
+      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
+      pbeg(p);
+      k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, p->tw3, N, 0);
+      k_ref_rows<L, REF_FWD><<<gn, E::NT, SM, p->stream>>>(p->Wr, nullptr, w + (size_t)r * N * N, nullptr, Hx, tw,
+                                                             p->tw3, N, 1.f, 0);
+      pend(p, HOLO_PASS_REF, A * 2.0 + 8.0 * N * N, fl * (L + N));
+    }
+  }
+
   static void run(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc) {
     const int N = p->N, R = p->n_ref;
     const size_t SM = E::SMEM;
@@ -812,6 +834,23 @@ holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref, v
     case 2048: RefRun<2048>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
     case 4096: RefRun<4096>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
     case 6144: RefRun<6144>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
+  }
+  return postcheck(p);
+}
+
+holo_status holo_fwd_ref(holo_plan *p, const void *q, void *w) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!q || (p->n_ref > 0 && !w)) return fail(p, HOLO_EINVAL, "null pointer");
+  if (p->n_ref == 0) return HOLO_OK;
+  switch (p->L) {
+    case 128: RefRun<128>::fwd(p, (const float2 *)q, (float2 *)w); break;
+    case 256: RefRun<256>::fwd(p, (const float2 *)q, (float2 *)w); break;
+    case 512: RefRun<512>::fwd(p, (const float2 *)q, (float2 *)w); break;
+    case 1024: RefRun<1024>::fwd(p, (const float2 *)q, (float2 *)w); break;
+    case 2048: RefRun<2048>::fwd(p, (const float2 *)q, (float2 *)w); break;
+    case 4096: RefRun<4096>::fwd(p, (const float2 *)q, (float2 *)w); break;
+    case 6144: RefRun<6144>::fwd(p, (const float2 *)q, (float2 *)w); break;
   }
   return postcheck(p);
 }

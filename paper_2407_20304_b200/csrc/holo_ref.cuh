@@ -107,7 +107,7 @@ struct LineEng<6144> {
   }
 };
 
-enum { REF_QHAT = 0, REF_R1 = 1, REF_R2 = 2, REF_R3 = 3, REF_FINAL = 4 };
+enum { REF_QHAT = 0, REF_R1 = 1, REF_R2 = 2, REF_R3 = 3, REF_FINAL = 4, REF_FWD = 5 };
 
 // ---------------------------------------------------------------- column passes
 // QHAT : Qx (P2, spectral x / spatial y) -> forward along y -> Qhat (P2), in place
@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
 // R2   : W row (P2, N rows) x Hx -> inverse along x -> crop, residual (+F), pad ->
 //        forward along x -> x conj(Hx) -> V (P2, N rows); partial[blk] = F of the CTA
 // FINAL: Ghat row (P2) -> inverse along x -> out (row-major) (+)= scale v
+// FWD  : W row (P2, N rows) x Hx -> inverse along x -> crop -> w frame (row-major N x N)
 template <int L, int MODE>
 __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     k_ref_rows(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
@@ -219,6 +220,21 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
       for (int r = 0; r < 16; r++) {
         const int f = E::ifr(st, r);
         out[p2(y, f, N)] = cmulc(v[r], ldg2(Hx + f));
+      }
+    }
+  } else if (MODE == REF_FWD) {
+    const bool act = y < N;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int f = E::ifr(st, r);
+      v[r] = act ? cmul(ldg2(in + p2(y, f, N)), ldg2(Hx + f)) : make_float2(0.f, 0.f);
+    }
+    E::inv(v, st, tw, tw3);
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) {
+        const int c = E::isp(st, r) - o;
+        if (c >= 0 && c < N) out[(size_t)y * N + c] = v[r];
       }
     }
   } else {  // FINAL

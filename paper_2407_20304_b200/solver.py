@@ -18,14 +18,19 @@ import math
 import torch
 import torch.distributed as dist
 
-from . import HoloCgIn
+from . import HOLO_ACCUMULATE_Q, HoloCgIn
 
 
 class JointCG:
+    """Product-space Dai-Yuan CG over (psi_local..., q).  ``sqrt_dref`` (optional) adds the
+    reference arm (O14, holo_grad_ref) of this rank's reference frames to F and grad_q;
+    a plan with n_angles = 0 then runs the probe-only problem of configs[4] (rho_psi unused)."""
+
     def __init__(self, plan, sqrt_d, psi0, q0, rho_psi=1.0, rho_q=1.0, gamma_init=1.0, max_halvings=12,
-                 group=None, distributed=None):
+                 group=None, distributed=None, sqrt_dref=None):
         self.plan = plan
         self.d = sqrt_d
+        self.dref = sqrt_dref
         self.rho = (float(rho_psi), float(rho_q))
         self.gamma_init, self.max_halvings = float(gamma_init), int(max_halvings)
         self.group = group
@@ -38,6 +43,7 @@ class JointCG:
         self.g_psi, self.g_q = z(self.psi), z(self.q)
         self.gt_psi, self.gt_q = z(self.psi), z(self.q)
         self.sc = torch.zeros(5, dtype=torch.float64, device=dev)
+        self.scr = torch.zeros(1, dtype=torch.float64, device=dev)  # F of the reference arm
         self.F = None
         self.dots = None
         self.g_eta = 0.0          # Re<g_m, eta_{m-1}>
@@ -52,7 +58,13 @@ class JointCG:
         """F and grad at (psi, q); returns host (F, gg_psi, geta_psi, gg_q, geta_q)."""
         p = self.plan
         sc3 = self.sc[:3]
-        p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
+        if p.K > 0:
+            p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
+        else:
+            sc3.zero_()
+        if self.dref is not None:  # reference arm: F_ref into sc[0], its gradient added to g_q
+            p.grad_ref(q, self.dref, self.scr, g_q, flags=HOLO_ACCUMULATE_Q if p.K > 0 else 0)
+            sc3[:1] += self.scr
         if self.dist:
             # exchange 1: probe-gradient partial (complex64 viewed as float32), exchange 2: scalars
             dist.all_reduce(torch.view_as_real(g_q), group=self.group)
