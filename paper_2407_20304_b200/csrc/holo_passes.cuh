@@ -158,6 +158,14 @@ __global__ void __launch_bounds__(NT, 1)
   const bool act = y < N;
   const int o = (L - N) / 2;
   float2 v[16];
+  float dv[16];  // sqrt_d of this thread's crop positions, fetched before the transforms
+  if (MODE == X2_GRAD || MODE == X2_OBJ) {
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int c = t + r * T - o;
+      dv[r] = (act && c >= 0 && c < N) ? __ldg(sqrt_d + (size_t)y * N + c) : 0.f;
+    }
+  }
   if (MODE != X2_ADJ) {
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = act ? ldg2(in + p2(y, t + r * T, N)) : make_float2(0.f, 0.f);
@@ -182,7 +190,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int c = t + r * T - o;
       float2 w = make_float2(0.f, 0.f);
       if (act && c >= 0 && c < N) {
-        const float d = __ldg(sqrt_d + (size_t)y * N + c);
+        const float d = dv[r];
         const float m = sqrtf(v[r].x * v[r].x + v[r].y * v[r].y);
         const float dm = m - d;
         acc += (double)(dm * dm);
@@ -290,6 +298,8 @@ __global__ void __launch_bounds__(NT, 1)
   for (int j = 0; j < nz; j++) {
     const float2 *T3j = T3 + (size_t)j * L * L;
     if ((magmask >> j) & 1u) {
+      // source re-read from global (L2) for the second half; the first half is parked privately
+      // (loading the row once into the private slot measured 3% slower)
       mag_adj<L>(
           v, [&](int r) { return ldg2(T3j + p2(y, t + r * T, L)); }, [&](int r, float2 e) { Z[r] = e; },
           [&](int r) { return Z[r]; }, pipe, seq, j > 0, x, t, tb.tw);
