@@ -794,12 +794,15 @@ holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float 
                       void *grad_psi, void *grad_q_part, double *sc, uint32_t flags) {
   holo_status st = precheck(p);
   if (st != HOLO_OK) return st;
-  if (!psi || !q || !sqrt_d || !sc) return fail(p, HOLO_EINVAL, "null pointer");
+  const int K = p->K, nz = p->nz, N = p->N, L = p->L;
+  if (!q || !sc || (K > 0 && (!psi || !sqrt_d))) return fail(p, HOLO_EINVAL, "null pointer");
   if (flags & HOLO_ACCUMULATE_Q) return fail(p, HOLO_EUNSUPPORTED, "HOLO_ACCUMULATE_Q not implemented for holo_grad");
   const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0;
-  const int K = p->K, nz = p->nz, N = p->N, L = p->L;
   HC(cudaMemsetAsync(sc, 0, 3 * sizeof(double), p->stream));
-  if (K == 0) return HOLO_OK;
+  if (K == 0) {  // empty shard: F = 0 and a zero probe-gradient partial (sums over no angles)
+    if (!obj && grad_q_part) HC(cudaMemsetAsync(grad_q_part, 0, sizeof(float2) * (size_t)L * L, p->stream));
+    return HOLO_OK;
+  }
   dispatch_sweep<Run>(p, obj ? 3 : 0, (const float2 *)psi, (const float2 *)q, sqrt_d, (const float2 *)nullptr,
                       (float2 *)nullptr, (const float2 *)eta_psi_prev, obj ? nullptr : (float2 *)grad_psi,
                       obj ? nullptr : (float2 *)grad_q_part, 2.0f, !obj && grad_q_part != nullptr);
