@@ -103,6 +103,8 @@ holo_status holo_adj(holo_plan *p, const void *y /*[K][nz][n][n]*/, const void *
 
 #define HOLO_ACCUMULATE_Q 1u  /* add into grad_q_part instead of overwriting          */
 #define HOLO_OBJECTIVE_ONLY 2u /* F only: no adjoint work, grad outputs ignored       */
+#define HOLO_INTENSITY 4u      /* holo_grad: intensity objective F_2 (tau = 2, Eq. (9)):
+                                  F = sum (|w|^2 - sqrt_d^2)^2, rho = 2 (|w|^2 - sqrt_d^2) w (App. A.3)  */
 
 /* Fused sweep at (psi, q) over this plan's angles (O8-O12; Eqs. (10)-(12)).
  * Writes fp64 DEVICE scalars sc[3]:

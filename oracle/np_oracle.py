@@ -116,18 +116,25 @@ class Problem:
         a = self.mag(j).fwd(psi_k, s[0], s[1])
         return crop(prop(qj * a, self.g.wavelength, self.g.p0, self.g.zdet[j]), self.N), a
 
-    def frame_grad(self, psi_k, qj, j, s, sqrt_d):
-        """One frame (k, j): returns F_kj, 2 L_kj^* rho, and conj(a) v (the G_j term, no 2, no P_{-omega})."""
+    def frame_grad(self, psi_k, qj, j, s, sqrt_d, tau=1):
+        """One frame (k, j): returns F_kj, 2 L_kj^* rho, and conj(a) v (the G_j term, no 2, no P_{-omega}).
+        tau = 1: F_1 (Eq. (10)), rho = w - sqrt_d w/|w|;  tau = 2: F_2 (Eq. (9)), F = (|w|^2 - d)^2,
+        rho = h'(|w|^2) w = 2 (|w|^2 - d) w  (App. A.3 proposition with h(t) = (t - d)^2)."""
         w, a = self.frame_fwd(psi_k, qj, j, s)
         m = np.abs(w)
-        F = float(np.sum((m - sqrt_d) ** 2))
-        with np.errstate(invalid="ignore", divide="ignore"):
-            rho = np.where(m > 0, w - sqrt_d * w / np.where(m > 0, m, 1), 0)
+        if tau == 2:
+            dm = m ** 2 - sqrt_d ** 2
+            F = float(np.sum(dm ** 2))
+            rho = 2.0 * dm * w
+        else:
+            F = float(np.sum((m - sqrt_d) ** 2))
+            with np.errstate(invalid="ignore", divide="ignore"):
+                rho = np.where(m > 0, w - sqrt_d * w / np.where(m > 0, m, 1), 0)
         v = prop(zpad(rho, self.L), self.g.wavelength, self.g.p0, -self.g.zdet[j])
         gpsi = 2.0 * self.mag(j).adj(np.conj(qj) * v, s[0], s[1])
         return F, gpsi, np.conj(a) * v
 
-    def grad(self, psi, q, shifts, sqrt_d, frames=None):
+    def grad(self, psi, q, shifts, sqrt_d, frames=None, tau=1):
         """F, grad_psi, grad_q over all frames (or a subset: list of (k, j))."""
         K, nz = psi.shape[0], self.g.nz
         frames = frames if frames is not None else [(k, j) for j in range(nz) for k in range(K)]
@@ -138,7 +145,7 @@ class Problem:
         for (k, j) in frames:
             if j not in qjs:
                 qjs[j] = self.qj(q, j)
-            Fk, gk, Gk = self.frame_grad(psi[k], qjs[j], j, shifts[k, j], sqrt_d[k, j])
+            Fk, gk, Gk = self.frame_grad(psi[k], qjs[j], j, shifts[k, j], sqrt_d[k, j], tau)
             F += Fk
             gpsi[k] += gk
             G[j] = G.get(j, 0) + Gk

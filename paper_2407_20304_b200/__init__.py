@@ -20,6 +20,7 @@ from . import _build
 HOLO_OK, HOLO_EINVAL, HOLO_ENOMEM, HOLO_ECUDA, HOLO_EUNSUPPORTED, HOLO_ESTATE = 0, -1, -2, -3, -4, -5
 HOLO_ACCUMULATE_Q = 1
 HOLO_OBJECTIVE_ONLY = 2
+HOLO_INTENSITY = 4  # F_2 (tau = 2)
 HOLO_MAX_NZ = 8
 
 LIB_PATH = os.environ.get("HOLO_LIB", _build.LIB)  # HOLO_LIB: a tuning-variant build of the same sources

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(NT, 1)
 template <int L, int MODE>
 __global__ void __launch_bounds__(NT, 1)
     k_x2(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
-         double *__restrict__ partial, Tables tb, const __grid_constant__ TabSeq seq, int N) {
+         double *__restrict__ partial, Tables tb, const __grid_constant__ TabSeq seq, int N, int tau2) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
@@ -191,11 +191,18 @@ __global__ void __launch_bounds__(NT, 1)
       float2 w = make_float2(0.f, 0.f);
       if (act && c >= 0 && c < N) {
         const float d = dv[r];
-        const float m = sqrtf(v[r].x * v[r].x + v[r].y * v[r].y);
-        const float dm = m - d;
-        acc += (double)(dm * dm);
-        const float f = m > 0.f ? 1.0f - __fdividef(d, m) : 0.f;  // rho = w - d w/|w|, 0 at w = 0 (C7)
-        w = cscale(v[r], f);
+        const float m2 = v[r].x * v[r].x + v[r].y * v[r].y;
+        if (tau2) {  // F_2 (tau = 2, Eq. (9)): (|w|^2 - d~)^2, rho = h'(|w|^2) w = 2 (|w|^2 - d~) w
+          const float dm = m2 - d * d;
+          acc += (double)dm * (double)dm;
+          w = cscale(v[r], 2.0f * dm);
+        } else {  // F_1 (tau = 1, Eq. (10)): (|w| - sqrt d~)^2, rho = w - sqrt(d~) w/|w|, 0 at w = 0 (C7)
+          const float m = sqrtf(m2);
+          const float dm = m - d;
+          acc += (double)(dm * dm);
+          const float f = m > 0.f ? 1.0f - __fdividef(d, m) : 0.f;
+          w = cscale(v[r], f);
+        }
       }
       v[r] = w;
     }

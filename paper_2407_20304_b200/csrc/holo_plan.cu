@@ -41,7 +41,8 @@ struct holo_plan {
   // workspace
   float2 *T1 = nullptr, *Aw = nullptr, *W1 = nullptr, *V1 = nullptr, *T3 = nullptr, *G = nullptr, *QJ = nullptr;
   double *partF = nullptr, *partX3 = nullptr, *partQ = nullptr;
-  int nbx2 = 0, nbx3 = 0;  // CTAs of the X2 / X3 launches (partials per frame / per angle)
+  int nbx2 = 0, nbx3 = 0;
+  int tau2 = 0;  // objective of the current holo_grad call: 0 = F_1 (amplitude), 1 = F_2 (intensity)  // CTAs of the X2 / X3 launches (partials per frame / per angle)
   size_t ws_bytes = 0;
   std::vector<void *> allocs;
   std::string err;
@@ -376,20 +377,20 @@ struct Run {
         if (mode == 0) qh.p[qh.n++] = p->hdet + (size_t)j * L;
         pbeg(p);
         if (mode == 1) {
-          k_x2<L, X2_FWD><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, qh, N);
+          k_x2<L, X2_FWD><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, qh, N, p->tau2);
           pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
           continue;
         }
         if (mode == 3) {
-          k_x2<L, X2_OBJ><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, qh, N);
+          k_x2<L, X2_OBJ><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, qh, N, p->tau2);
           pend(p, HOLO_PASS_X2, rN * A + NN8 / 2, N * fl * 2);
           continue;
         }
         if (mode == 0) {
-          k_x2<L, X2_GRAD><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, qh, N);
+          k_x2<L, X2_GRAD><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, qh, N, p->tau2);
           pend(p, HOLO_PASS_X2, 2 * rN * A + NN8 / 2, N * fl * 4);
         } else {
-          k_x2<L, X2_ADJ><<<nbx2, NT, SM::XT, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, qh, N);
+          k_x2<L, X2_ADJ><<<nbx2, NT, SM::XT, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, qh, N, p->tau2);
           pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
         }
         float2 *Gj = want_q ? p->G + (size_t)j * LL : nullptr;
@@ -798,6 +799,7 @@ holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float 
   if (!q || !sc || (K > 0 && (!psi || !sqrt_d))) return fail(p, HOLO_EINVAL, "null pointer");
   if (flags & HOLO_ACCUMULATE_Q) return fail(p, HOLO_EUNSUPPORTED, "HOLO_ACCUMULATE_Q not implemented for holo_grad");
   const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0;
+  p->tau2 = (flags & HOLO_INTENSITY) ? 1 : 0;
   HC(cudaMemsetAsync(sc, 0, 3 * sizeof(double), p->stream));
   if (K == 0) {  // empty shard: F = 0 and a zero probe-gradient partial (sums over no angles)
     if (!obj && grad_q_part) HC(cudaMemsetAsync(grad_q_part, 0, sizeof(float2) * (size_t)L * L, p->stream));

@@ -198,3 +198,19 @@ def test_full_size_one_angle_parity(name):
     p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, gpsi, gqd)
     assert abs(host(sc).real[0] - F) / F < TOL_S
     assert rel(host(gpsi), gp) < TOL_G and rel(host(gqd), gq) < TOL_G
+
+
+@pytest.mark.parametrize("name,K", [("cfg0", 4), ("cfg1", 2)])
+def test_intensity_objective_f2_parity(name, K):
+    """HOLO_INTENSITY: F_2 (tau = 2, Eq. (9)) and its gradients vs the numpy oracle (tau = 2)."""
+    import paper_2407_20304_b200 as hb
+    c = Case(name, K, oracle_kind="np")
+    p = make_plan(c.cfg, c.K)
+    p.set_shifts(c.s)
+    F, gp, gq = npo.Problem(c.g, c.cfg.npad, c.cfg.n).grad(c.psi, c.q, c.s, c.d, tau=2)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, gpsi, gqd, flags=hb.HOLO_INTENSITY)
+    assert abs(host(sc).real[0] - F) / F < TOL_S
+    assert rel(host(gpsi), gp) < TOL_G and rel(host(gqd), gq) < TOL_G

@@ -432,3 +432,30 @@ def test_o14_numpy_reference_arm_equals_c_oracle():
     Fn, gn = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs, d)
     assert abs(Fn - Fc) / Fc < 1e-12
     assert rel(gn, gc) < 1e-11
+
+
+def test_f2_intensity_objective_finite_differences():
+    """F_2 (tau = 2, Eq. (9)) in the numpy oracle: central finite differences of F_2
+    in psi and q directions equal Re<v, grad F_2> (App. A.3 proposition), and F_2 = 0, grad = 0
+    at exact intensity data."""
+    cfg = synth.CONFIGS["cfg0"]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    L, N, K = 16, 8, 2
+    rng = np.random.default_rng(22)
+    psi = np.exp(1j * 0.3 * rng.standard_normal((K, L, L)))
+    q = 1 + 0.2 * (rng.standard_normal((L, L)) + 1j * rng.standard_normal((L, L)))
+    s = rng.uniform(-2, 2, size=(K, 2, 2))
+    pr = npo.Problem(g, L, N)
+    out = pr.fwd(psi, q, s)
+    d_exact = np.stack([np.stack([np.abs(out[(k, j)]) for j in range(2)]) for k in range(K)])
+    F0, gp0, gq0 = pr.grad(psi, q, s, d_exact, tau=2)
+    assert F0 < 1e-20 and np.abs(gp0).max() < 1e-10 and np.abs(gq0).max() < 1e-10
+    d = d_exact * (1 + 0.3 * rng.standard_normal(d_exact.shape))
+    F, gp, gq = pr.grad(psi, q, s, d, tau=2)
+    h = 1e-6
+    vp = rng.standard_normal(psi.shape) + 1j * rng.standard_normal(psi.shape)
+    fd = (pr.grad(psi + h * vp, q, s, d, tau=2)[0] - pr.grad(psi - h * vp, q, s, d, tau=2)[0]) / (2 * h)
+    assert abs(fd - np.vdot(gp, vp).real) / abs(fd) < 1e-6
+    vq = rng.standard_normal(q.shape) + 1j * rng.standard_normal(q.shape)
+    fd = (pr.grad(psi, q + h * vq, s, d, tau=2)[0] - pr.grad(psi, q - h * vq, s, d, tau=2)[0]) / (2 * h)
+    assert abs(fd - np.vdot(gq, vq).real) / abs(fd) < 1e-6
