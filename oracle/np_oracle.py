@@ -166,7 +166,7 @@ class Problem:
         return out
 
 
-def grad_ref(wavelength, p0, zeta0, q, ref_shifts, sqrt_dref, want_q=True):
+def grad_ref(wavelength, p0, zeta0, q, ref_shifts, sqrt_dref, want_q=True, tau=1):
     """O14 (reference constraint P:102; Eq. (10) reference term P:115; Eq. (12)),
     numpy.fft as the DFT:  w_r = C(P_{zeta0} S_{s_r} q),  F = sum_r || |w_r| - sqrt_dref_r ||^2,
     grad_q = 2 sum_r S_{-s_r} P_{-zeta0} Z rho_r,  rho = w - a w/|w| (0 at w = 0)."""
@@ -179,8 +179,13 @@ def grad_ref(wavelength, p0, zeta0, q, ref_shifts, sqrt_dref, want_q=True):
         w = crop(prop(shift(q, sx, sy), wavelength, p0, zeta0), N)
         a = np.asarray(sqrt_dref[r], np.float64)
         m = np.abs(w)
-        F += float(np.sum((m - a) ** 2))
-        if want_q:
+        if tau == 2:  # F_2 reference term (Eq. (9)): (|w|^2 - d)^2, rho = 2 (|w|^2 - d) w
+            dm = m ** 2 - a ** 2
+            F += float(np.sum(dm ** 2))
+            rho = 2.0 * dm * w
+        else:
+            F += float(np.sum((m - a) ** 2))
             rho = np.where(m > 0, w - a * w / np.where(m > 0, m, 1.0), 0.0)
+        if want_q:
             gq += 2.0 * shift(prop(zpad(rho, L), wavelength, p0, -zeta0), -sx, -sy)
     return F, gq

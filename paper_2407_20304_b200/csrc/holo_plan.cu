@@ -502,7 +502,8 @@ struct RefRun {
       pbeg(p);
       k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, tw3, N, 0);
       k_ref_rows<L, REF_R2><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r * N * N, p->Vr,
-                                                            p->partR + (size_t)r * gn, Hx, tw, tw3, N, 1.f, 0);
+                                                            p->partR + (size_t)r * gn, Hx, tw, tw3, N, 1.f, 0,
+                                                            p->tau2);
       if (gq) k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, tw3, N, r == 0);
       pend(p, HOLO_PASS_REF, A * (1.0 + 0.5 + 0.5 + 1.0 / 8 + 0.5 + (gq ? 0.5 + (r ? 2.0 : 1.0) : 0.0)),
            fl * (L + 2.0 * N + (gq ? L : 0)));
@@ -826,6 +827,7 @@ holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref, v
   if (!q || !sc || (p->n_ref > 0 && !sqrt_dref)) return fail(p, HOLO_EINVAL, "null pointer");
   HC(cudaMemsetAsync(sc, 0, sizeof(double), p->stream));
   const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0, acc = (flags & HOLO_ACCUMULATE_Q) != 0;
+  p->tau2 = (flags & HOLO_INTENSITY) ? 1 : 0;
   float2 *gq = obj ? nullptr : (float2 *)grad_q_part;
   if (p->n_ref == 0) {
     if (gq && !acc) HC(cudaMemsetAsync(gq, 0, sizeof(float2) * (size_t)p->L * p->L, p->stream));

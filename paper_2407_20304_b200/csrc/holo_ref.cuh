@@ -175,7 +175,7 @@ template <int L, int MODE>
 __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     k_ref_rows(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
                double *__restrict__ partial, const float2 *__restrict__ Hx, const float4 *__restrict__ tw,
-               const float2 *__restrict__ tw3, int N, float scale, int accumulate) {
+               const float2 *__restrict__ tw3, int N, float scale, int accumulate, int tau2 = 0) {
   using E = LineEng<L>;
   extern __shared__ float4 sm4[];
   __shared__ double red[32];
@@ -204,11 +204,18 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
       float2 w = make_float2(0.f, 0.f);
       if (act && c >= 0 && c < N) {
         const float d = __ldg(sqrt_d + (size_t)y * N + c);
-        const float m = sqrtf(v[r].x * v[r].x + v[r].y * v[r].y);
-        const float dm = m - d;
-        acc += (double)(dm * dm);
-        const float f = m > 0.f ? 1.0f - __fdividef(d, m) : 0.f;  // O9 / reading C7
-        w = cscale(v[r], f);
+        const float m2 = v[r].x * v[r].x + v[r].y * v[r].y;
+        if (tau2) {  // F_2 reference term (Eq. (9)): (|w|^2 - d~)^2, rho = 2 (|w|^2 - d~) w
+          const float dm = m2 - d * d;
+          acc += (double)dm * (double)dm;
+          w = cscale(v[r], 2.0f * dm);
+        } else {  // F_1: O9 / reading C7
+          const float m = sqrtf(m2);
+          const float dm = m - d;
+          acc += (double)(dm * dm);
+          const float f = m > 0.f ? 1.0f - __fdividef(d, m) : 0.f;
+          w = cscale(v[r], f);
+        }
       }
       v[r] = w;
     }

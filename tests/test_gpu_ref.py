@@ -126,3 +126,21 @@ def test_fwd_ref_matches_oracle_forward():
         for r in range(R):
             wo = npo.crop(npo.prop(npo.shift(q, rs[r, 0], rs[r, 1]), g.wavelength, g.p0, g.zeta[0]), N)
             assert rel(wn[r], wo) < 2e-5, (L, r)
+
+
+def test_ref_arm_f2_parity():
+    """HOLO_INTENSITY on the reference arm: F_2 reference term and its q-gradient."""
+    import paper_2407_20304_b200 as hb
+    cfg = synth.CONFIGS["cfg4"]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    L, N, R = 256, 128, 3
+    q_t = synth.probe(cfg, L=L).numpy()
+    rs = np.random.default_rng(9).uniform(-8, 8, size=(R, 2))
+    d = ref_data(g, q_t, rs, N, 9)
+    q = 0.9 * q_t
+    F, gq = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs, d, tau=2)
+    p = plan(cfg, L, N)
+    p.set_ref_shifts(rs)
+    Fg, gg = run_gpu(p, q, d, flags=hb.HOLO_INTENSITY)
+    assert abs(Fg - F) / F < TOL_S
+    assert rel(gg, gq) < TOL_G

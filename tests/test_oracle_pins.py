@@ -459,3 +459,21 @@ def test_f2_intensity_objective_finite_differences():
     vq = rng.standard_normal(q.shape) + 1j * rng.standard_normal(q.shape)
     fd = (pr.grad(psi, q + h * vq, s, d, tau=2)[0] - pr.grad(psi, q - h * vq, s, d, tau=2)[0]) / (2 * h)
     assert abs(fd - np.vdot(gq, vq).real) / abs(fd) < 1e-6
+
+
+def test_f2_reference_arm_finite_differences():
+    """F_2 reference term (Eq. (9)) in np_oracle.grad_ref: central differences vs Re<v, grad>."""
+    cfg = synth.CONFIGS["cfg4"]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    L, N, R = 32, 16, 2
+    rng = np.random.default_rng(23)
+    q = 1 + 0.2 * (rng.standard_normal((L, L)) + 1j * rng.standard_normal((L, L)))
+    rs = rng.uniform(-5, 5, size=(R, 2))
+    d = np.abs(rng.standard_normal((R, N, N)))
+    F, gq = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs, d, tau=2)
+    h = 1e-6
+    v = rng.standard_normal(q.shape) + 1j * rng.standard_normal(q.shape)
+    Fp = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q + h * v, rs, d, False, tau=2)[0]
+    Fm = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q - h * v, rs, d, False, tau=2)[0]
+    fd = (Fp - Fm) / (2 * h)
+    assert abs(fd - np.vdot(gq, v).real) / abs(fd) < 1e-6
