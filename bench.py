@@ -50,6 +50,64 @@ def peaks():
         return 6650.0, 1965.0, "fallback"
 
 
+def fp32_peak(device):
+    """P_FP32 measured by the in-repo FFMA microbenchmark (tools/fp32peak.cu), with the SM clock
+    it ran at; falls back to the nominal 148 SM x 128 lanes x 2 x max clock if the tool is absent."""
+    import ctypes
+    lib = os.path.join(ROOT, "tools", "libfp32peak.so")
+    try:
+        if not os.path.exists(lib):
+            import __graft_entry__
+            __graft_entry__.build_tools()
+        f = ctypes.CDLL(lib).fp32_peak
+        f.argtypes = [ctypes.c_int, ctypes.c_double] + [ctypes.POINTER(ctypes.c_double)] * 3
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        if f(device, 60.0, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)) == 0 and a.value > 0:
+            return {"ffma_tflops": a.value, "ffma_fadd_tflops": b.value, "sm_mhz": c.value,
+                    "source": "measured: tools/fp32peak.cu (FFMA chains, 148 x 8 CTAs x 256 threads)"}
+    except Exception as e:  # pragma: no cover
+        print(f"fp32 microbenchmark unavailable: {e}", file=sys.stderr)
+    _, mhz, _ = peaks()
+    return {"ffma_tflops": N_SM * FP32_LANES_PER_SM * 2 * mhz * 1e6 / 1e12, "ffma_fadd_tflops": None,
+            "sm_mhz": mhz, "source": "nominal 148 SM x 128 lanes x 2 x max clock"}
+
+
+# SURVEY 8(a) algorithmic HBM bytes per frame and pass, in units of A = 8 L^2 (N_z = 4 schedule;
+# X1 counts the psi / eta / g state I/O of the CG step amortised over the planes).  B_min = sum.
+ALG_BYTES_A = {"X1": 2.25, "Y1": 1.5, "X2": 1.125, "Y2": 2.5, "X3": 1.5}
+B_MIN_A = 8.875
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def c_oracle_frames():
+    """The naive-DFT C oracle (oracle/holo_oracle.c, OpenMP, fp64) timed per frame on all 8 frames
+    of cfg0 and 8 frames (2 angles x 4 planes) of cfg1 -- SURVEY 8(d)'s oracle timing."""
+    import oracle
+    out = {}
+    for name, K in (("cfg0", 4), ("cfg1", 2)):
+        cfg = synth.CONFIGS[name]
+        g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+        psi = synth.psi_stack(cfg, K=K).numpy()
+        q = synth.probe(cfg).numpy()
+        s = synth.shifts(cfg, K=K)
+        d = np.abs(oracle.fwd(g, psi, q, s, cfg.n))
+        t0 = time.perf_counter()
+        oracle.grad(g, np.ones_like(psi), 0.9 * q, s, d)
+        dt = time.perf_counter() - t0
+        out[name] = {"frames": K * cfg.nz, "s_per_frame": dt / (K * cfg.nz),
+                     "frame_it_per_s": K * cfg.nz / dt}
+    return out
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
 
@@ -125,9 +183,10 @@ def cpu_baseline(cfg, k=0, j=1):
     t0 = time.perf_counter()
     pr.frame_grad(np.ones_like(psi_t[0]), qj, j, s[0, j], d)
     dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"1 frame (k={k}, j={j}) of {cfg.name}: F + grad_psi + grad_q term on the "
-                      f"{cfg.npad}^2 torus, numpy/BLAS fp64 oracle (oracle/np_oracle.py); {dt:.2f} s"}
+                      f"{cfg.npad}^2 torus, numpy/BLAS fp64 oracle (oracle/np_oracle.py); {dt:.2f} s",
+            "c_oracle_naive_dft": c_oracle_frames()}
 
 
 def run_reference(args):
@@ -265,6 +324,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rho-q", type=float, default=None)
+    ap.add_argument("--batch", type=int, default=8, help="angle_batch of the plan (angles per Y1/X2/Y2 launch)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -285,7 +345,8 @@ def main():
         K_total = 0
     else:
         cfg, K, k0, scaling = workload(args.workload, world, rank, args.angles)
-        plan = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=local)
+        plan = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=local,
+                       angle_batch=min(args.batch, K))
         plan.set_shifts(synth.shifts(cfg)[k0:k0 + K] if k0 + K <= cfg.n_angles else
                         np.resize(synth.shifts(cfg), (k0 + K, cfg.nz, 2))[k0:k0 + K])
         # ---- synthetic measurement: |forward(truth)|^2 with Poisson noise (bench input, not a parity value)
@@ -308,7 +369,8 @@ def main():
         conf = {"workload": f"{cfg.name}: {cfg.n}^2 projections on a {cfg.npad}^2 torus, {cfg.nz} distances, "
                             f"{K} angles per GPU ({K_total} total)",
                 "angles_per_gpu": K, "angles_total": K_total, "distances": cfg.nz, "n": cfg.n,
-                "npad": cfg.npad, "rho_q": rho_q, "parallelism": f"angle-sharded dp{world}",
+                "npad": cfg.npad, "rho_q": rho_q, "angle_batch": plan.angle_batch,
+                "parallelism": f"angle-sharded dp{world}",
                 "l2": "inputs > L2 (each step streams >= 25 GB per GPU; no flush needed)"}
     solver.start()
     for _ in range(args.warmup):
@@ -349,41 +411,77 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    value = frames * args.steps / (ms / 1e3)
+    accepted = sum(1 for h in hist if h["gamma"] > 0)
+    # metric: accepted CG iterations only (a line-search failure, gamma = 0, still costs its sweeps)
+    value = frames * accepted / (ms / 1e3)
 
-    # ---- roofline of the dominant kernel (CUDA events on the plan's stream, same region)
+    # ---- roofline.  Per pass, from the CUDA events of the profiled run:
+    #   algorithmic bytes = 8(a)'s per-frame figure x frames, flops = the implemented schedule's
+    #   5 L log2 L count; the binding roof of a pass is max(bytes / BW, flops / P_FP32).
     bw, sm_mhz_max, src = peaks()
-    fp32_peak = N_SM * FP32_LANES_PER_SM * 2 * sm_mhz_max * 1e6 / 1e12  # TFLOP/s
-    top = max(prof, key=lambda k: prof[k]["ms"])
+    fp = fp32_peak(local)
+    p32 = fp["ffma_tflops"]
+    A = 8.0 * cfg.npad ** 2
+    prof_frames = (solver.sweeps - sw0 - sweeps) * (K_total // world) * cfg.nz if K_total else 0
+    passes = {}
+    for k, v in prof.items():
+        if not v["launches"]:
+            continue
+        sec = v["ms"] / 1e3
+        e = {"ms_per_step": v["ms"] / args.steps, "launches": v["launches"],
+             "model_GBps": v["bytes"] / sec / 1e9, "TFLOPs": v["flops"] / sec / 1e12,
+             "fp32_frac": v["flops"] / sec / 1e12 / p32}
+        if k in ALG_BYTES_A and prof_frames:
+            ab = ALG_BYTES_A[k] * A * prof_frames
+            e.update({"alg_bytes_per_frame": ALG_BYTES_A[k] * A, "alg_GBps": ab / sec / 1e9,
+                      "hbm_frac": ab / sec / 1e9 / bw,
+                      "binding_frac": max(ab / (bw * 1e9), v["flops"] / (p32 * 1e12)) / sec,
+                      "us_per_frame": 1e6 * sec / prof_frames, "flops_per_frame": v["flops"] / prof_frames})
+        passes[k] = e
+    chain = [k for k in ALG_BYTES_A if k in passes]
+    top = max(chain or passes, key=lambda k: prof[k]["ms"])
     P = prof[top]
-    sec = P["ms"] / 1e3
-    gbs = P["bytes"] / sec / 1e9
-    tfs = P["flops"] / sec / 1e12
-    t_hbm, t_alu = P["bytes"] / (bw * 1e9), P["flops"] / (fp32_peak * 1e12)
+    nl = max(P["launches"], 1)
+    launch_s = P["ms"] / 1e3 / nl
+    fl_launch = P["flops"] / nl
+    frames_per_launch = prof_frames / nl if (top in ALG_BYTES_A and prof_frames) else None
+    by_launch = ALG_BYTES_A.get(top, 0) * A * frames_per_launch if frames_per_launch else P["bytes"] / nl
+    t_hbm, t_alu = by_launch / (bw * 1e9), fl_launch / (p32 * 1e12)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(top)
+            tj = json.load(open(tfile))
+            if tj.get("_workload") == cfg.name and top in tj:  # ncu dram bytes per launch of the same launch shape
+                traffic = tj[top]
         except Exception:
             traffic = None
     if t_hbm >= t_alu:
-        roof = {"bound": "hbm", "achieved": gbs, "peak": bw, "unit": "GB/s", "frac": gbs / bw, "traffic": traffic}
+        roof = {"bound": "hbm", "achieved": by_launch / launch_s / 1e9, "peak": bw, "unit": "GB/s"}
     else:
-        roof = {"bound": "alu", "achieved": tfs, "peak": fp32_peak, "unit": "TFLOP/s", "frac": tfs / fp32_peak,
-                "traffic": traffic}
-    roof.update({"kernel": top, "peak_source": f"{src} (hbm {bw:.0f} GB/s; fp32 = 148 SM x 128 x 2 x "
-                 f"{sm_mhz_max:.0f} MHz)", "share_of_step": P["ms"] / ms_prof,
-                 "bytes_per_launch": P["bytes"] / max(P["launches"], 1),
-                 "flops_per_launch": P["flops"] / max(P["launches"], 1),
-                 "launch_us": 1e3 * P["ms"] / max(P["launches"], 1)})
-    tot_bytes = sum(v["bytes"] for v in prof.values())
+        roof = {"bound": "alu", "achieved": fl_launch / launch_s / 1e12, "peak": p32, "unit": "TFLOP/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof.update({"traffic": traffic, "kernel": top,
+                 "peak_source": f"hbm: {src} MEASURED_PEAKS.json {bw:.0f} GB/s; fp32: {fp['source']} "
+                                f"{p32:.1f} TFLOP/s at {fp['sm_mhz']:.0f} MHz",
+                 "alg_bytes_per_launch": by_launch, "flops_per_launch": fl_launch,
+                 "frames_per_launch": frames_per_launch, "launch_us": 1e6 * launch_s,
+                 "hbm_frac": by_launch / launch_s / 1e9 / bw, "fp32_frac": fl_launch / launch_s / 1e12 / p32,
+                 "traffic_over_alg": (traffic / by_launch) if traffic else None,
+                 "share_of_step": P["ms"] / ms_prof})
+    # step level: T_roof = frames x max(B_min / BW, F_alg / P_FP32) against the measured step
+    f_alg = sum(passes[k].get("flops_per_frame", 0) for k in chain)
+    t_frame = (ms / 1e3) / (frames * max(accepted, 1) / max(args.steps, 1)) if frames else None
+    step = None
+    if frames and f_alg:
+        t_roof = max(B_MIN_A * A / (bw * 1e9), f_alg / (p32 * 1e12))
+        step = {"B_min_bytes_per_frame": B_MIN_A * A, "F_alg_flops_per_frame": f_alg,
+                "T_roof_us_per_frame": 1e6 * t_roof, "T_meas_us_per_frame": 1e6 * t_frame,
+                "binding_frac": t_roof / t_frame,
+                "binding": "fp32" if f_alg / (p32 * 1e12) > B_MIN_A * A / (bw * 1e9) else "hbm",
+                "hbm_frac_B_min": B_MIN_A * A * value / 1e9 / bw,
+                "hbm_frac_B_min_8TBps": B_MIN_A * A * value / 1e9 / 8000.0}
     prof_overhead = ms_prof / ms - 1.0
-    passes = {k: {"ms_per_step": v["ms"] / args.steps, "launches": v["launches"],
-                  "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0,
-                  "TFLOPs": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 else 0}
-              for k, v in prof.items() if v["launches"]}
-
     # ---- e2e: same metric through the public API with the step's input (sqrt d) copied
     #      from pinned host memory every step and the step's result (F) read back
     e2e = None
@@ -421,9 +519,10 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "c64 (fp32 complex; fp64 reductions)", "data": "synthetic",
             "config": conf,
-            "sweeps_per_step": sweeps / args.steps,
+            "iterations": args.steps, "accepted_iterations": accepted,
+            "sweeps_per_step": sweeps / args.steps, "sweeps_per_s": sweeps / (ms / 1e3),
             "F_last": hist[-1]["F"], "gamma_last": hist[-1]["gamma"],
-            "hbm_frac_step": (tot_bytes / (ms_prof / 1e3) / 1e9) / bw,
+            "roofline_step": step, "fp32_peak": fp,
             "profiled_steps_overhead": prof_overhead,
             "roofline": roof, "passes": passes, "gpu_launches": int(launches),
             "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,

@@ -49,6 +49,7 @@ typedef enum {
 } holo_status;
 
 #define HOLO_MAX_NZ 8
+#define HOLO_MAX_BATCH 16
 
 /* Acquisition geometry (Table 1; Eq. (6); Eq. (8)). */
 typedef struct {
@@ -57,7 +58,11 @@ typedef struct {
                           (6144 = 3*2^11 for reference-arm-only plans, n_angles == 0)          */
   int32_t nz;          /* number of sample planes ("distances"), 1..HOLO_MAX_NZ               */
   int32_t n_angles;    /* K: angles resident on this device (0: reference-arm-only plan)      */
-  int32_t angle_batch; /* reserved (sizes future batched workspace); pass 1                   */
+  int32_t angle_batch; /* B, 1..HOLO_MAX_BATCH: angles whose frames of one plane share a Y1 /
+                          X2 / Y2 launch (q_j read once and the probe-gradient accumulator G_j
+                          read-modify-written once per batch, Eq. (12)).  Sizes the
+                          workspace: ~ (2 nz + 2) B npad^2 complex64.  Results do not depend on B
+                          beyond fp32 rounding of the G_j sum order.                          */
   double wavelength;   /* lambda [m] > 0                                                       */
   double focus_to_detector; /* Z [m]                                                          */
   double z1[HOLO_MAX_NZ];   /* focus-to-sample [m], 0 < z1[0] < ... < z1[nz-1] < Z            */

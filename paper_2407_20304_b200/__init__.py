@@ -22,6 +22,7 @@ HOLO_ACCUMULATE_Q = 1
 HOLO_OBJECTIVE_ONLY = 2
 HOLO_INTENSITY = 4  # F_2 (tau = 2)
 HOLO_MAX_NZ = 8
+HOLO_MAX_BATCH = 16
 
 LIB_PATH = os.environ.get("HOLO_LIB", _build.LIB)  # HOLO_LIB: a tuning-variant build of the same sources
 if not os.path.exists(LIB_PATH):
@@ -88,7 +89,7 @@ _lib.holo_profile_read.restype = _S
 
 HOLO_NPASS = 9
 PASS_NAMES = ["X1", "Y1", "X2", "Y2", "X3", "filter", "reduce", "cg", "ref"]
-PASS_KERNELS = ["k_x1", "k_y1", "k_x2", "k_y2", "k_x3", "k_rows_filter|k_cols_filter|k_scale_add",
+PASS_KERNELS = ["k_x1", "k_y1", "k_x2", "k_y2", "k_x3", "k_rows_filter|k_cols_filter|k_p2_convert",
                 "k_reduce|k_dots", "k_cg", "k_ref"]
 
 EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes", "holo_last_error",
@@ -123,7 +124,9 @@ class Plan:
     """holo_plan_create: one (device, stream) plan for K angles x nz planes on an npad^2 torus."""
 
     def __init__(self, n, npad, z1, n_angles, wavelength, focus_to_detector, detector_pixel, device=0,
-                 stream=None, angle_batch=1):
+                 stream=None, angle_batch=None):
+        if angle_batch is None:  # default: 8 angles per Y1/X2/Y2 launch (DESIGN.md "Angle batching")
+            angle_batch = max(1, min(8, n_angles))
         g = HoloGeometry()
         g.n, g.npad, g.nz, g.n_angles, g.angle_batch = n, npad, len(z1), n_angles, angle_batch
         g.wavelength, g.focus_to_detector, g.detector_pixel = wavelength, focus_to_detector, detector_pixel
@@ -140,6 +143,8 @@ class Plan:
             raise HoloError(st, "holo_plan_create failed")
         self._h = h
         self.n, self.npad, self.nz, self.K = n, npad, len(z1), n_angles
+        self.angle_batch = angle_batch
+        self.n_ref = 0
         self.geometry = g
 
     def __del__(self):
@@ -189,6 +194,7 @@ class Plan:
     def set_ref_shifts(self, s):
         s = np.ascontiguousarray(s, dtype=np.float64).reshape(-1, 2)
         self._chk(_lib.holo_set_ref_shifts(self._h, s.shape[0], s.ctypes.data_as(_P)))
+        self.n_ref = s.shape[0]
 
     # ---- hot path
     def fwd(self, psi, q, w):
@@ -217,14 +223,14 @@ class Plan:
 
     def grad_ref(self, q, sqrt_dref, sc, grad_q_part=None, flags=0):
         self._chk(_lib.holo_grad_ref(self._h, _ptr(q, torch.complex64, self.npad ** 2, "q"),
-                                     _ptr(sqrt_dref, torch.float32, None, "sqrt_dref"),
+                                     _ptr(sqrt_dref, torch.float32, self.n_ref * self.n ** 2, "sqrt_dref"),
                                      _ptr(grad_q_part, torch.complex64, self.npad ** 2, "grad_q_part"),
                                      _ptr(sc, torch.float64, 1, "sc"), flags))
 
     def fwd_ref(self, q, w):
         """holo_fwd_ref: w[r] = C(P_{zeta0} S_{s_r} q) for the n_ref reference frames."""
         self._chk(_lib.holo_fwd_ref(self._h, _ptr(q, torch.complex64, self.npad ** 2, "q"),
-                                    _ptr(w, torch.complex64, None, "w")))
+                                    _ptr(w, torch.complex64, self.n_ref * self.n ** 2, "w")))
         return w
 
     def q_dots(self, grad_q, eta_q_prev, out):

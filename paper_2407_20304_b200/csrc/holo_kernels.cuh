@@ -19,7 +19,7 @@
 //   spectrum X = FFT(x);  a[i] = cr[f] X[f],  i = (f + L/2) mod L   (register r -> r^8)
 //   cr = kappa (-1)^fbar e^{i pi mt fbar^2/L} r_s[f] / L   (chirp x shift ramp, per (k, j, axis))
 //   E = IFFT(FFT(a) Bhat_e),  O = IFFT(FFT(a w) Bhat_o),  w[i] = e^{-i pi i/L}
-//   y[o] = cout[o] E[o] + cwo[o] O[o],   cout = e^{i pi mt (o-L/2)^2/L},  cwo = cout conj(w)
+//   y[o] = cout[o] (E[o] + conj(w[o]) O[o]),   cout = e^{i pi mt (o-L/2)^2/L}
 // i.e. the 2L-point cyclic convolution with b[d] = e^{-i pi mt d^2/L} split into its
 // even/odd spectral halves.  The adjoint runs the same steps conjugated and in reverse.
 // All tables are fp64-generated on the host, phases reduced in cycles.
@@ -34,10 +34,8 @@ struct Tables {
   const float2 *hdet;   // [nz][L] h_{zdet_j}[f] / L
   const float2 *homega; // [nz][L] h_{omega_j}[f] (unscaled)
   const float2 *cout;   // [nz][L] e^{i pi mt (o - L/2)^2 / L}
-  const float2 *cwo;    // [nz][L] cout[o] conj(w[o])
   const float2 *bke;    // [nz][L] Bhat[2k] / (2L)
   const float2 *bko;    // [nz][L] Bhat[2k+1] / (2L)
-  const float2 *wodd;   // [L] e^{-i pi i / L}
   const float2 *cr;     // [K][nz][2][L] spectrum factor per (k, j, axis): mag: cin r_s, else r_s / L
 };
 
@@ -114,11 +112,16 @@ __device__ __forceinline__ void mul_tab(float2 (&v)[16], const float2 *__restric
 // by 1-D bulk copies (cp.async.bulk + mbarrier), each issued one transform ahead of
 // its use: the FFT hides the L2 latency that a direct load would expose.  The
 // launch's table sequence is a kernel parameter (built on the host).
-constexpr int MAXTAB = 40;
+constexpr int MAXTAB = 160;  // a batched launch chains the tables of up to 16 frames
 struct TabSeq {
   const float2 *p[MAXTAB];
   int n;
 };
+
+// L2 prefetch of a contiguous block (16-byte aligned, multiple of 16 bytes)
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

@@ -51,6 +51,31 @@ __device__ __forceinline__ void st_p2_col(const float2 (&v)[16], float2 *__restr
 
 // ----------------------------------------------------------------------------- X1
 // rows of psi_k (row-major):  X = FFT(psi row) (kept thread-private); per j: T1_j row = M_{1/mt_j} S_{sx} psi row
+// (one non-inlined call per plane: only pointers and the pipe state cross it, so the
+// magnification keeps the whole register budget)
+template <int L>
+__device__ __noinline__ void x1_plane(float2 *__restrict__ T1j, const float4 *__restrict__ tw, const TabSeq &seq,
+                                      TabPipe<L> &pipe, float2 *sm, bool mag, bool sync0) {
+  using C = CtaK<L>;
+  Xch x = C::xch(sm);
+  const Priv<NT> X{priv_base<L>(sm)};
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  float2 v[16];
+  if (mag) {
+    // X (thread-private smem) is reused by every plane: the first half's term stays in registers
+    float2 e[16];
+    mag_fwd<L>(
+        v, [&](int r) { return X[r]; }, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe, seq,
+        sync0, x, t, tw);
+  } else {
+    const float2 *cr = pipe.take(seq, sync0);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmul(X[r], cr[t + r * (L / 16)]);
+    fft<L, true>(v, x, t, tw);
+  }
+  st_p2_row<L>(v, T1j, y, L, t);
+}
+
 template <int L>
 __global__ void __launch_bounds__(NT, 1)
     k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1, Tables tb, const __grid_constant__ TabSeq seq,
@@ -59,92 +84,105 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
-  Xch x = C::xch(sm);
-  const Priv<NT> X{priv_base<L>(sm)};
   TabPipe<L> pipe;
   pipe.start(seq, slot_base<L, true>(sm), bars);
-  const int t = C::t(), y = blockIdx.x * C::G + C::g();
-  float2 v[16];
-  ld_row<L>(v, psi_k + (size_t)y * L, t);
-  fft<L, false>(v, x, t, tb.tw);
+  {
+    Xch x = C::xch(sm);
+    const Priv<NT> X{priv_base<L>(sm)};
+    const int t = C::t(), y = blockIdx.x * C::G + C::g();
+    float2 v[16];
+    ld_row<L>(v, psi_k + (size_t)y * L, t);
+    fft<L, false>(v, x, t, tb.tw);
 #pragma unroll
-  for (int r = 0; r < 16; r++) X[r] = v[r];
-  for (int j = 0; j < nz; j++) {
-    if ((magmask >> j) & 1u) {
-      // X (thread-private smem) is reused by every plane: the first half's term stays in registers
-      float2 e[16];
-      mag_fwd<L>(
-          v, [&](int r) { return X[r]; }, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe,
-          seq, j > 0, x, t, tb.tw);
-    } else {
-      const float2 *cr = pipe.take(seq, j > 0);
-#pragma unroll
-      for (int r = 0; r < 16; r++) v[r] = cmul(X[r], cr[t + r * (L / 16)]);
-      fft<L, true>(v, x, t, tb.tw);
-    }
-    st_p2_row<L>(v, T1 + (size_t)j * L * L, y, L, t);
+    for (int r = 0; r < 16; r++) X[r] = v[r];
   }
+#pragma unroll 1
+  for (int j = 0; j < nz; j++) x1_plane<L>(T1 + (size_t)j * L * L, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j > 0);
 }
 
 // ----------------------------------------------------------------------------- Y1
-// columns of T1_j:  a = M_{1/mt_j} S_{sy} (column);  optionally store a;
-// optionally  W1 = rows [o, o+N) of D_y(q_j . a)   (W1: P2 with N rows)
+// Angle-batched (Eq. (12)'s sum over k is what makes a batch pay): nb frames of ONE plane
+// j, frame b at T1j + b * fstride.  Each CTA owns G columns and loops over the batch, so
+// its q_j columns are re-read from L2, and the next frame's input block (contiguous in P2)
+// is prefetched into L2 by a bulk copy while the current frame is transformed.
+// Per frame: a = M_{1/mt_j} S_{sy} (column) -> Aout[b] (optional);
+//            W1[b] = rows [o, o+N) of D_y(q_j . a) (optional; P2 with N rows)
+// The frame body is a separate (non-inlined) function: only the loop state crosses the
+// call, so the transforms keep the full register budget (an inlined loop spills).
 template <int L>
-__global__ void __launch_bounds__(NT, 1)
-    k_y1(const float2 *__restrict__ T1j, const float2 *__restrict__ qj, float2 *__restrict__ Aout,
-         float2 *__restrict__ W1, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N) {
+__device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float2 *__restrict__ qj,
+                                      float2 *__restrict__ aout, float2 *__restrict__ w1, const float4 *__restrict__ tw,
+                                      const TabSeq &seq, TabPipe<L> &pipe, float2 *sm, int mag, int N) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
-  extern __shared__ float4 sm4[];
-  __shared__ uint64_t bars[2];
-  float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
   const Priv<NT> X{priv_base<L>(sm)};
-  TabPipe<L> pipe;
-  pipe.start(seq, slot_base<L, true>(sm), bars);
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
   float2 v[16];
-  ld_p2_col<L>(v, T1j, col, L, t);
-  fft<L, false>(v, x, t, tb.tw);
+  ld_p2_col<L>(v, in, col, L, t);
+  fft<L, false>(v, x, t, tw);
   if (mag) {
 #pragma unroll
     for (int r = 0; r < 16; r++) X[r] = v[r];
     mag_fwd<L>(
         v, [&](int r) { return X[r]; }, [&](int r, float2 e) { X[r] = e; }, [&](int r) { return X[r]; }, pipe, seq,
-        false, x, t, tb.tw);
+        false, x, t, tw);
   } else {
     const float2 *cr = pipe.take(seq);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], cr[t + r * T]);
-    fft<L, true>(v, x, t, tb.tw);
+    fft<L, true>(v, x, t, tw);
   }
-  if (Aout) st_p2_col<L>(v, Aout, col, L, t);
-  if (W1) {
+  if (aout) st_p2_col<L>(v, aout, col, L, t);
+  if (w1) {
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + p2(t + r * T, col, L)));
-    fft<L, false>(v, x, t, tb.tw);
+    fft<L, false>(v, x, t, tw);
     const float2 *h = pipe.take(seq);  // hdet_j / L
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], h[t + r * T]);
-    fft<L, true>(v, x, t, tb.tw);
+    fft<L, true>(v, x, t, tw);
     const int o = (L - N) / 2;
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const int row = t + r * T - o;
-      if (row >= 0 && row < N) W1[p2(row, col, N)] = v[r];
+      if (row >= 0 && row < N) w1[p2(row, col, N)] = v[r];
     }
   }
 }
 
+template <int L>
+__global__ void __launch_bounds__(NT, 1)
+    k_y1(const float2 *__restrict__ T1j, size_t fstride, const float2 *__restrict__ qj, float2 *__restrict__ Aout,
+         float2 *__restrict__ W1, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
+  using C = CtaK<L>;
+  extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  TabPipe<L> pipe;
+  pipe.start(seq, slot_base<L, true>(sm), bars);
+  const int col0 = blockIdx.x * C::G;
+#pragma unroll 1
+  for (int b = 0; b < nb; b++) {
+    const float2 *in = T1j + (size_t)b * fstride;
+    if (threadIdx.x == 0 && b + 1 < nb) prefetch_l2(in + fstride + p2(0, col0, L), 8u * C::G * L);
+    y1_frame<L>(in, qj, Aout ? Aout + (size_t)b * L * L : nullptr, W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq,
+                pipe, sm, mag, N);
+  }
+}
+
 // ----------------------------------------------------------------------------- X2
-// rows y < N.  GRAD: W1 row -> D_x, crop, residual (+F), pad, D_x^* -> V1   (W1, V1: P2, N rows)
-//              FWD : W1 row -> D_x, crop -> w frame [N][N] (row-major)
-//              ADJ : y frame row (row-major) -> pad, D_x^* -> V1
-//              OBJ : W1 row -> D_x, crop, F only
+// rows y < N of frame b = blockIdx.y of an nb-frame batch (one plane, so one table set).
+//   GRAD: W1 row -> D_x, crop, residual (+F), pad, D_x^* -> V1   (W1, V1: P2, N rows)
+//   FWD : W1 row -> D_x, crop -> w frame [N][N] (row-major)
+//   ADJ : y frame row (row-major) -> pad, D_x^* -> V1
+//   OBJ : W1 row -> D_x, crop, F only
+// Strides between the batch's frames: in / out (elements), sqrt_d (elements), partial (CTAs).
 template <int L, int MODE>
 __global__ void __launch_bounds__(NT, 1)
-    k_x2(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
-         double *__restrict__ partial, Tables tb, const __grid_constant__ TabSeq seq, int N, int tau2) {
+    k_x2(const float2 *__restrict__ in, size_t in_stride, const float *__restrict__ sqrt_d, size_t d_stride,
+         float2 *__restrict__ out, size_t out_stride, double *__restrict__ partial, int part_stride, Tables tb,
+         const __grid_constant__ TabSeq seq, int N, int tau2) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
@@ -154,6 +192,11 @@ __global__ void __launch_bounds__(NT, 1)
   Xch x = C::xch(sm);
   TabPipe<L> pipe;  // hdet_j / L (GRAD: twice)
   pipe.start(seq, slot_base<L, false>(sm), bars);
+  const int fb = blockIdx.y;
+  in += fb * in_stride;
+  out += fb * out_stride;
+  if (sqrt_d) sqrt_d += fb * d_stride;
+  partial += (size_t)fb * part_stride;
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   const bool act = y < N;
   const int o = (L - N) / 2;
@@ -225,44 +268,43 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // ----------------------------------------------------------------------------- Y2
-// columns:  v = D_y^* pad(V1 col);  G_j += conj(a) v;  T3_j = (M S)_y^*(conj(q_j) v)
+// Angle-batched like Y1: nb frames of plane j; frame b reads V1 + b N L, a + b L L and
+// writes T3j + b * fstride.  The probe-gradient accumulator G_j (Eq. (12)) is
+// read-modify-written once per frame by the SAME CTA for its columns, so across the
+// batch it stays in L2 (DRAM sees ~one read + one write per batch).
+// Per frame:  v = D_y^* pad(V1 col);  G_j += conj(a) v;  T3j = (M S)_y^*(conj(q_j) v)
 template <int L>
-__global__ void __launch_bounds__(NT, 1)
-    k_y2(const float2 *__restrict__ V1, const float2 *__restrict__ a, const float2 *__restrict__ qj,
-         float2 *__restrict__ Gj, float2 *__restrict__ T3j, Tables tb, const __grid_constant__ TabSeq seq, int mag,
-         int N) {
+__device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const float2 *__restrict__ ab,
+                                      const float2 *__restrict__ qj, float2 *__restrict__ Gj, float2 *__restrict__ t3,
+                                      const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> &pipe, float2 *sm,
+                                      int mag, int N) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
-  extern __shared__ float4 sm4[];
-  __shared__ uint64_t bars[2];
-  float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
   const Priv<NT> Y{priv_base<L>(sm)};
-  TabPipe<L> pipe;
-  pipe.start(seq, slot_base<L, true>(sm), bars);
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
   const int o = (L - N) / 2;
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; r++) {
     const int row = t + r * T - o;
-    v[r] = (row >= 0 && row < N) ? ldg2(V1 + p2(row, col, N)) : make_float2(0.f, 0.f);
+    v[r] = (row >= 0 && row < N) ? ldg2(vin + p2(row, col, N)) : make_float2(0.f, 0.f);
   }
-  fft<L, false>(v, x, t, tb.tw);
+  fft<L, false>(v, x, t, tw);
   {
     const float2 *h = pipe.take(seq);  // hdet_j / L, conjugated
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], h[t + r * T]);
   }
-  fft<L, true>(v, x, t, tb.tw);
+  fft<L, true>(v, x, t, tw);
   if (Gj) {
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const size_t gi = p2(t + r * T, col, L);
-      Gj[gi] = cadd(Gj[gi], cmulc(v[r], ldg2(a + gi)));
+      Gj[gi] = cadd(Gj[gi], cmulc(v[r], ldg2(ab + gi)));
     }
   }
-  if (!T3j) return;
+  if (!t3) return;
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));
   if (mag) {
@@ -270,20 +312,81 @@ __global__ void __launch_bounds__(NT, 1)
     for (int r = 0; r < 16; r++) Y[r] = v[r];
     mag_adj<L>(
         v, [&](int r) { return Y[r]; }, [&](int r, float2 e) { Y[r] = e; }, [&](int r) { return Y[r]; }, pipe, seq,
-        true, x, t, tb.tw);
+        true, x, t, tw);
   } else {
-    fft<L, false>(v, x, t, tb.tw);
+    fft<L, false>(v, x, t, tw);
     const float2 *cr = pipe.take(seq);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
   }
-  fft<L, true>(v, x, t, tb.tw);
-  st_p2_col<L>(v, T3j, col, L, t);
+  fft<L, true>(v, x, t, tw);
+  st_p2_col<L>(v, t3, col, L, t);
+}
+
+template <int L>
+__global__ void __launch_bounds__(NT, 1)
+    k_y2(const float2 *__restrict__ V1, const float2 *__restrict__ a, const float2 *__restrict__ qj,
+         float2 *__restrict__ Gj, float2 *__restrict__ T3j, size_t fstride, Tables tb,
+         const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
+  using C = CtaK<L>;
+  extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  TabPipe<L> pipe;
+  pipe.start(seq, slot_base<L, true>(sm), bars);
+  const int col0 = blockIdx.x * C::G;
+#pragma unroll 1
+  for (int b = 0; b < nb; b++) {
+    const float2 *vin = V1 + (size_t)b * N * L;
+    const float2 *ab = a + (size_t)b * L * L;
+    if (threadIdx.x == 0 && b + 1 < nb) {
+      prefetch_l2(vin + (size_t)N * L + p2(0, col0, N), 8u * C::G * N);
+      if (Gj) prefetch_l2(ab + (size_t)L * L + p2(0, col0, L), 8u * C::G * L);
+    }
+    y2_frame<L>(vin, ab, qj, Gj, T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N);
+  }
 }
 
 // ----------------------------------------------------------------------------- X3
 // rows: g_k row = scale * IFFT( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3_j row;
 // partial[blk][0] = sum |g|^2, partial[blk][1] = sum Re(g conj(eta))   (g, eta row-major)
+// The sum over planes is kept in the g row itself (L2-resident between planes); each plane
+// is one non-inlined call (spill-free magnification).
+template <int L>
+__device__ __noinline__ void x3_plane(const float2 *__restrict__ T3j, float2 *__restrict__ grow,
+                                      const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> &pipe, float2 *sm,
+                                      bool mag, int j, bool last) {
+  using C = CtaK<L>;
+  constexpr int T = L / 16;
+  Xch x = C::xch(sm);
+  const Priv<NT> Z{priv_base<L>(sm)};
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  float2 v[16];
+  if (mag) {
+    // source re-read from global (L2) for the second half; the first half is parked privately
+    mag_adj<L>(
+        v, [&](int r) { return ldg2(T3j + p2(y, t + r * T, L)); }, [&](int r, float2 e) { Z[r] = e; },
+        [&](int r) { return Z[r]; }, pipe, seq, j > 0, x, t, tw);
+  } else {
+    ld_p2_row<L>(v, T3j, y, L, t);
+    fft<L, false>(v, x, t, tw);
+    const float2 *cr = pipe.take(seq);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
+  }
+  if (j > 0) {
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cadd(grow[t + r * T], v[r]);
+  }
+  if (last) {
+#pragma unroll
+    for (int r = 0; r < 16; r++) Z[r] = v[r];  // the summed spectrum, for the final transform
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; r++) grow[t + r * T] = v[r];
+  }
+}
+
 template <int L>
 __global__ void __launch_bounds__(NT, 1)
     k_x3(const float2 *__restrict__ T3, const float2 *__restrict__ eta, float2 *__restrict__ g,
@@ -295,36 +398,18 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ double red[32];
   __shared__ uint64_t bars[2];
   float2 *sm = reinterpret_cast<float2 *>(sm4);
-  Xch x = C::xch(sm);
-  const Priv<NT> Z{priv_base<L>(sm)};
   TabPipe<L> pipe;
   pipe.start(seq, slot_base<L, true>(sm), bars);
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 *grow = g + (size_t)y * L;  // also the Fourier-domain accumulator of sum_j W_j
+#pragma unroll 1
+  for (int j = 0; j < nz; j++)
+    x3_plane<L>(T3 + (size_t)j * L * L, grow, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j, j + 1 == nz);
+  Xch x = C::xch(sm);
+  const Priv<NT> Z{priv_base<L>(sm)};
   float2 v[16];
-  for (int j = 0; j < nz; j++) {
-    const float2 *T3j = T3 + (size_t)j * L * L;
-    if ((magmask >> j) & 1u) {
-      // source re-read from global (L2) for the second half; the first half is parked privately
-      // (loading the row once into the private slot measured 3% slower)
-      mag_adj<L>(
-          v, [&](int r) { return ldg2(T3j + p2(y, t + r * T, L)); }, [&](int r, float2 e) { Z[r] = e; },
-          [&](int r) { return Z[r]; }, pipe, seq, j > 0, x, t, tb.tw);
-    } else {
-      ld_p2_row<L>(v, T3j, y, L, t);
-      fft<L, false>(v, x, t, tb.tw);
-      const float2 *cr = pipe.take(seq);
 #pragma unroll
-      for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
-    }
-    if (j + 1 < nz) {
-#pragma unroll
-      for (int r = 0; r < 16; r++) grow[t + r * T] = j == 0 ? v[r] : cadd(grow[t + r * T], v[r]);
-    } else if (j > 0) {
-#pragma unroll
-      for (int r = 0; r < 16; r++) v[r] = cadd(grow[t + r * T], v[r]);
-    }
-  }
+  for (int r = 0; r < 16; r++) v[r] = Z[r];
   fft<L, true>(v, x, t, tb.tw);
   double gg = 0.0, ge = 0.0;
 #pragma unroll
@@ -404,7 +489,7 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 // layout conversion (plane without propagation, omega_j = 0):  P2 <-> row-major, out (+)= scale * in
-__global__ void k_p2_convert(const float2 *__restrict__ in, float2 *__restrict__ out, int L, int to_p2, float scale,
+static __global__ void k_p2_convert(const float2 *__restrict__ in, float2 *__restrict__ out, int L, int to_p2, float scale,
                              int accumulate) {
   const size_t n = (size_t)L * L;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -416,17 +501,9 @@ __global__ void k_p2_convert(const float2 *__restrict__ in, float2 *__restrict__
   }
 }
 
-// ------------------------------------------------------------------ pointwise / reductions
-__global__ void k_scale_add(const float2 *__restrict__ in, float2 *__restrict__ out, size_t n, float scale,
-                            int accumulate) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    float2 v = cscale(in[i], scale);
-    out[i] = accumulate ? cadd(out[i], v) : v;
-  }
-}
-
+// ------------------------------------------------------------------ reductions
 // deterministic single-block sum: out[v] = sum_i partial[i * nval + v], v < nval
-__global__ void k_reduce(const double *__restrict__ partial, size_t n, int nval, double *__restrict__ out,
+static __global__ void k_reduce(const double *__restrict__ partial, size_t n, int nval, double *__restrict__ out,
                          int accumulate) {
   __shared__ double red[32];
   for (int v = 0; v < nval; v++) {
@@ -439,7 +516,7 @@ __global__ void k_reduce(const double *__restrict__ partial, size_t n, int nval,
 }
 
 // partial dots over n complex: part[b][0] = sum |x|^2, part[b][1] = sum Re(x conj(y))
-__global__ void k_dots(const float2 *__restrict__ x, const float2 *__restrict__ y, size_t n, double *__restrict__ part) {
+static __global__ void k_dots(const float2 *__restrict__ x, const float2 *__restrict__ y, size_t n, double *__restrict__ part) {
   __shared__ double red[32];
   double a = 0.0, b = 0.0;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -460,7 +537,7 @@ __global__ void k_dots(const float2 *__restrict__ x, const float2 *__restrict__ 
 
 // CG pointwise step (Eq. (13)-(14)): mode 0: eta = -rho g; 1: eta = -rho g + beta eta; 2: keep eta.
 // xt = x + gamma eta.  Two complex per thread-iteration (float4).
-__global__ void k_cg(const float4 *__restrict__ x, float4 *__restrict__ eta, const float4 *__restrict__ g,
+static __global__ void k_cg(const float4 *__restrict__ x, float4 *__restrict__ eta, const float4 *__restrict__ g,
                      float4 *__restrict__ xt, size_t n4, float rho, float beta, float gamma, int mode) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
     float4 e;

@@ -1,5 +1,6 @@
-// holo_plan.cu -- host side of libholo: plan, fp64 table generation, argument
-// validation, pass orchestration and the C ABI of include/holo.h.
+// holo_plan.cu -- host side of libholo: plan creation, fp64 table generation, argument
+// validation and the C ABI of include/holo.h.  The per-L pass runners live in
+// inst_<L>.cu (holo_run.cuh); this unit only dispatches through HoloOps.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -9,69 +10,31 @@
 #include <string>
 #include <vector>
 
-#include "../../include/holo.h"
-#include "holo_passes.cuh"
-#include "holo_ref.cuh"
+#include "holo_impl.cuh"
+#include "holo_passes.cuh"  // only the non-template helpers (k_reduce, k_dots, k_cg) are instantiated here
 
 using namespace holo;
 using cd = std::complex<double>;
 
+extern const HoloOps holo_ops_128, holo_ops_256, holo_ops_512, holo_ops_1024, holo_ops_2048, holo_ops_4096,
+    holo_ops_6144;
+
+const HoloOps *holo_ops_for(int L) {
+  switch (L) {
+    case 128: return &holo_ops_128;
+    case 256: return &holo_ops_256;
+    case 512: return &holo_ops_512;
+    case 1024: return &holo_ops_1024;
+    case 2048: return &holo_ops_2048;
+    case 4096: return &holo_ops_4096;
+    case 6144: return &holo_ops_6144;
+  }
+  return nullptr;
+}
+
 namespace {
 
 constexpr double kPi = 3.14159265358979323846264338327950288;
-
-struct Buf {
-  void *p = nullptr;
-  size_t bytes = 0;
-};
-
-}  // namespace
-
-struct holo_plan {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  holo_geometry g{};
-  int L = 0, N = 0, nz = 0, K = 0;
-  double m0 = 0, p0 = 0, mt[HOLO_MAX_NZ]{}, zeta[HOLO_MAX_NZ]{}, zdet[HOLO_MAX_NZ]{}, omega[HOLO_MAX_NZ]{};
-  uint32_t magmask = 0;
-  // device tables
-  float2 *tw = nullptr, *hdet = nullptr, *homega = nullptr, *cout = nullptr, *cwo = nullptr, *bke = nullptr,
-         *bko = nullptr, *wodd = nullptr, *cr = nullptr;
-  std::vector<std::complex<double>> cin_host;  // [nz][L] kappa (-1)^fbar e^{i pi mt fbar^2/L} / L
-  // workspace
-  float2 *T1 = nullptr, *Aw = nullptr, *W1 = nullptr, *V1 = nullptr, *T3 = nullptr, *G = nullptr, *QJ = nullptr;
-  double *partF = nullptr, *partX3 = nullptr, *partQ = nullptr;
-  int nbx2 = 0, nbx3 = 0;
-  int tau2 = 0;  // objective of the current holo_grad call: 0 = F_1 (amplitude), 1 = F_2 (intensity)  // CTAs of the X2 / X3 launches (partials per frame / per angle)
-  size_t ws_bytes = 0;
-  std::vector<void *> allocs;
-  std::string err;
-  bool sticky = false;
-  uint64_t launches = 0;
-  int n_ref = 0;
-  std::vector<double> ref_shifts;
-  // reference arm (holo_ref.cuh): Qhat, Ghat (P2, L x L), Wr, Vr (P2, N x L), Href [R][2][L], F partials
-  float2 *Qhat = nullptr, *Ghat = nullptr, *Wr = nullptr, *Vr = nullptr, *Href = nullptr, *tw3 = nullptr;
-  double *partR = nullptr;
-  int ref_cap = 0;  // frames Href / partR are sized for
-  // per-pass event profiling (holo_profile_*)
-  struct Rec { int id; double bytes, flops; size_t ev; };
-  bool prof_on = false;
-  std::vector<cudaEvent_t> evpool;
-  size_t evused = 0;
-  std::vector<Rec> recs;
-  double pms[HOLO_NPASS]{}, pbytes[HOLO_NPASS]{}, pflops[HOLO_NPASS]{};
-  uint64_t pcnt[HOLO_NPASS]{};
-
-  Tables tables() const {
-    Tables t;
-    t.tw = reinterpret_cast<const float4 *>(tw); t.hdet = hdet; t.homega = homega; t.cout = cout; t.cwo = cwo;
-    t.bke = bke; t.bko = bko; t.wodd = wodd; t.cr = cr;
-    return t;
-  }
-};
-
-namespace {
 
 holo_status fail(holo_plan *p, holo_status s, const std::string &msg) {
   if (p) p->err = msg;
@@ -100,9 +63,23 @@ holo_status dalloc(holo_plan *p, T **ptr, size_t bytes) {
     return fail(p, HOLO_ENOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
   }
   p->allocs.push_back(q);
+  p->alloc_bytes.push_back(bytes);
   p->ws_bytes += bytes;
   *ptr = reinterpret_cast<T *>(q);
   return HOLO_OK;
+}
+
+void dfree(holo_plan *p, void **ptr) {  // free one workspace buffer and forget it
+  if (!*ptr) return;
+  for (size_t i = 0; i < p->allocs.size(); i++)
+    if (p->allocs[i] == *ptr) {
+      p->ws_bytes -= p->alloc_bytes[i];
+      p->allocs.erase(p->allocs.begin() + i);
+      p->alloc_bytes.erase(p->alloc_bytes.begin() + i);
+      break;
+    }
+  cudaFree(*ptr);
+  *ptr = nullptr;
 }
 
 holo_status upload(holo_plan *p, float2 *dst, const std::vector<cd> &v) {
@@ -163,281 +140,6 @@ bool supported_L(int L) {
 // (configs[4], reading C16) serves reference-arm-only plans (n_angles = 0)
 bool chain_L(int L) { return (L & (L - 1)) == 0; }
 
-template <int L>
-struct Smem {
-  static constexpr size_t X = CtaK<L>::XBYTES;                      // exchange space only (filters)
-  static constexpr size_t XT = X + TabPipe<L>::BYTES;                // + two table slots
-  static constexpr size_t XPT = X + CtaK<L>::PRIV + TabPipe<L>::BYTES;  // + one thread-private line
-};
-
-template <int L>
-void set_smem_attrs() {
-  using S = Smem<L>;
-  auto a = [](const void *f, size_t s) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s); };
-  a((const void *)k_x1<L>, S::XPT);
-  a((const void *)k_y1<L>, S::XPT);
-  a((const void *)k_x2<L, X2_GRAD>, S::XT);
-  a((const void *)k_x2<L, X2_FWD>, S::XT);
-  a((const void *)k_x2<L, X2_ADJ>, S::XT);
-  a((const void *)k_x2<L, X2_OBJ>, S::XT);
-  a((const void *)k_y2<L>, S::XPT);
-  a((const void *)k_x3<L>, S::XPT);
-  a((const void *)k_rows_filter<L, false, true, false>, S::X);
-  a((const void *)k_rows_filter<L, true, false, false>, S::X);
-  a((const void *)k_rows_filter<L, true, false, true>, S::X);
-  a((const void *)k_cols_filter<L>, S::X);
-}
-
-template <int L>
-void set_ref_attrs() {
-  const int sz = (int)LineEng<L>::SMEM;
-  auto a = [&](const void *f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sz); };
-  a((const void *)k_ref_cols<L, REF_QHAT>);
-  a((const void *)k_ref_cols<L, REF_R1>);
-  a((const void *)k_ref_cols<L, REF_R3>);
-  a((const void *)k_ref_cols<L, REF_FINAL>);
-  a((const void *)k_ref_rows<L, REF_QHAT>);
-  a((const void *)k_ref_rows<L, REF_R2>);
-  a((const void *)k_ref_rows<L, REF_FINAL>);
-  a((const void *)k_ref_rows<L, REF_FWD>);
-}
-
-void set_attrs(int L) {
-  switch (L) {
-    case 128: set_ref_attrs<128>(); break;
-    case 256: set_ref_attrs<256>(); break;
-    case 512: set_ref_attrs<512>(); break;
-    case 1024: set_ref_attrs<1024>(); break;
-    case 2048: set_ref_attrs<2048>(); break;
-    case 4096: set_ref_attrs<4096>(); break;
-    case 6144: set_ref_attrs<6144>(); return;
-  }
-  switch (L) {
-    case 128: set_smem_attrs<128>(); break;
-    case 256: set_smem_attrs<256>(); break;
-    case 512: set_smem_attrs<512>(); break;
-    case 1024: set_smem_attrs<1024>(); break;
-    case 2048: set_smem_attrs<2048>(); break;
-    case 4096: set_smem_attrs<4096>(); break;
-  }
-}
-
-// ------------------------------------------------------------------ profiling
-void prof_flush(holo_plan *p) {
-  if (p->recs.empty()) return;
-  cudaEventSynchronize(p->evpool[p->recs.back().ev + 1]);
-  for (const auto &r : p->recs) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, p->evpool[r.ev], p->evpool[r.ev + 1]);
-    p->pms[r.id] += ms;
-    p->pbytes[r.id] += r.bytes;
-    p->pflops[r.id] += r.flops;
-    p->pcnt[r.id]++;
-  }
-  p->recs.clear();
-  p->evused = 0;
-}
-
-void pbeg(holo_plan *p) {
-  if (!p->prof_on) return;
-  if (p->evused + 2 > 32768) prof_flush(p);
-  while (p->evpool.size() < p->evused + 2) {
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    p->evpool.push_back(e);
-  }
-  cudaEventRecord(p->evpool[p->evused], p->stream);
-}
-
-void pend(holo_plan *p, int id, double bytes, double flops) {
-  p->launches++;
-  if (!p->prof_on) return;
-  cudaEventRecord(p->evpool[p->evused + 1], p->stream);
-  p->recs.push_back({id, bytes, flops, p->evused});
-  p->evused += 2;
-}
-
-double fftf(int L) {  // 5 L log2 L flops per length-L complex FFT
-  int lg = 0;
-  while ((1 << lg) < L) lg++;
-  return 5.0 * L * lg;
-}
-
-// ------------------------------------------------------------------ pass runners
-template <int L>
-struct Run {
-  using SM = Smem<L>;
-  static constexpr int G = CtaK<L>::G;
-  static constexpr double A = 8.0 * L * L;  // bytes of one L x L complex64 array
-
-  // q_j = P_{omega_j} q (O6): row-major q -> P2 QJ_j
-  static void qj(holo_plan *p, const float2 *q) {
-    const Tables tb = p->tables();
-    for (int j = 0; j < p->nz; j++) {
-      float2 *dst = p->QJ + (size_t)j * L * L;
-      pbeg(p);
-      if (p->omega[j] == 0.0) {
-        k_p2_convert<<<1184, 256, 0, p->stream>>>(q, dst, L, 1, 1.0f, 0);
-        pend(p, HOLO_PASS_FILTER, 2 * A, 0);
-        continue;
-      }
-      k_rows_filter<L, false, true, false><<<L / G, NT, SM::X, p->stream>>>(q, dst, tb, p->homega + j * L, 0, 1.0f);
-      pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
-      pbeg(p);
-      k_cols_filter<L><<<L / G, NT, SM::X, p->stream>>>(dst, dst, tb, p->homega + j * L, 0, 1.0f);
-      pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
-    }
-  }
-
-  // g_q (+)= scale * sum_j P_{-omega_j} G_j   (G_j P2 -> row-major out)
-  static void gq(holo_plan *p, float2 *out, float scale, bool accumulate) {
-    const Tables tb = p->tables();
-    for (int j = 0; j < p->nz; j++) {
-      float2 *Gj = p->G + (size_t)j * L * L;
-      const bool acc = accumulate || j > 0;
-      pbeg(p);
-      if (p->omega[j] == 0.0) {
-        k_p2_convert<<<1184, 256, 0, p->stream>>>(Gj, out, L, 0, scale, acc ? 1 : 0);
-        pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 0);
-        continue;
-      }
-      k_cols_filter<L><<<L / G, NT, SM::X, p->stream>>>(Gj, Gj, tb, p->homega + j * L, 1, 1.0f);
-      pend(p, HOLO_PASS_FILTER, 2 * A, 2.0 * L * fftf(L));
-      pbeg(p);
-      if (acc)
-        k_rows_filter<L, true, false, true><<<L / G, NT, SM::X, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale);
-      else
-        k_rows_filter<L, true, false, false><<<L / G, NT, SM::X, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale);
-      pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 2.0 * L * fftf(L));
-    }
-  }
-
-  // mode: 0 grad, 1 fwd, 2 adj (y given), 3 objective only
-  static void sweep(holo_plan *p, int mode, const float2 *psi, const float2 *q, const float *sqrt_d,
-                    const float2 *yin, float2 *wout, const float2 *eta, float2 *gpsi, float2 *gq_out, float gscale,
-                    bool want_q) {
-    Tables tb = p->tables();
-    const int N = p->N, nz = p->nz, K = p->K;
-    const size_t LL = (size_t)L * L;
-    const int nbx2 = (N + G - 1) / G;
-    const double fl = fftf(L), rN = (double)N / L, NN8 = 8.0 * N * N;
-    int nmag = 0;
-    for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
-    qj(p, q);
-    if (want_q) cudaMemsetAsync(p->G, 0, sizeof(float2) * LL * nz, p->stream);
-    // table sequences of the pipelined pointwise steps (holo_kernels.cuh, TabPipe)
-    auto crp = [&](int k, int j, int ax) { return p->cr + ((size_t)(k * nz + j) * 2 + ax) * L; };
-    auto add_fwd = [&](TabSeq &q, int k, int j, int ax) {  // mag_fwd: cr, bke, cr, bko, cout
-      const float2 *c = crp(k, j, ax);
-      const float2 *list[5] = {c, p->bke + (size_t)j * L, c, p->bko + (size_t)j * L, p->cout + (size_t)j * L};
-      for (auto *e : list) q.p[q.n++] = e;
-    };
-    auto add_adj = [&](TabSeq &q, int k, int j, int ax) {  // mag_adj: cout, bke, cout, bko, cr
-      const float2 *c = p->cout + (size_t)j * L;
-      const float2 *list[5] = {c, p->bke + (size_t)j * L, c, p->bko + (size_t)j * L, crp(k, j, ax)};
-      for (auto *e : list) q.p[q.n++] = e;
-    };
-    for (int k = 0; k < K; k++) {
-      const float2 *psik = psi + (size_t)k * LL;
-      const bool need_fwd_chain = (mode != 2) || want_q;
-      if (need_fwd_chain) {
-        TabSeq q{};
-        for (int j = 0; j < nz; j++) {
-          if ((p->magmask >> j) & 1u)
-            add_fwd(q, k, j, 0);
-          else
-            q.p[q.n++] = crp(k, j, 0);
-        }
-        pbeg(p);
-        k_x1<L><<<L / G, NT, SM::XPT, p->stream>>>(psik, p->T1, tb, q, nz, p->magmask);
-        pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * (1 + 4 * nmag + (nz - nmag)));
-      }
-      for (int j = 0; j < nz; j++) {
-        const int mag = (p->magmask >> j) & 1;
-        const float2 *T1j = p->T1 + (size_t)j * LL;
-        const float2 *qjj = p->QJ + (size_t)j * LL;
-        const size_t fr = (size_t)k * nz + j;
-        if (need_fwd_chain) {
-          float2 *aout = want_q ? p->Aw : nullptr;
-          float2 *w1 = (mode == 2) ? nullptr : p->W1;
-          TabSeq q{};
-          if (mag)
-            add_fwd(q, k, j, 1);
-          else
-            q.p[q.n++] = crp(k, j, 1);
-          if (w1) q.p[q.n++] = p->hdet + (size_t)j * L;
-          pbeg(p);
-          k_y1<L><<<L / G, NT, SM::XPT, p->stream>>>(T1j, qjj, aout, w1, tb, q, mag, N);
-          pend(p, HOLO_PASS_Y1, A + (w1 ? A + rN * A : 0) + (aout ? A : 0),
-               L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0)));
-        }
-        double *pf = p->partF + fr * nbx2;
-        TabSeq qh{};
-        qh.p[qh.n++] = p->hdet + (size_t)j * L;
-        if (mode == 0) qh.p[qh.n++] = p->hdet + (size_t)j * L;
-        pbeg(p);
-        if (mode == 1) {
-          k_x2<L, X2_FWD><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, nullptr, wout + fr * N * N, pf, tb, qh, N, p->tau2);
-          pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
-          continue;
-        }
-        if (mode == 3) {
-          k_x2<L, X2_OBJ><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, sqrt_d + fr * N * N, nullptr, pf, tb, qh, N, p->tau2);
-          pend(p, HOLO_PASS_X2, rN * A + NN8 / 2, N * fl * 2);
-          continue;
-        }
-        if (mode == 0) {
-          k_x2<L, X2_GRAD><<<nbx2, NT, SM::XT, p->stream>>>(p->W1, sqrt_d + fr * N * N, p->V1, pf, tb, qh, N, p->tau2);
-          pend(p, HOLO_PASS_X2, 2 * rN * A + NN8 / 2, N * fl * 4);
-        } else {
-          k_x2<L, X2_ADJ><<<nbx2, NT, SM::XT, p->stream>>>(yin + fr * N * N, nullptr, p->V1, pf, tb, qh, N, p->tau2);
-          pend(p, HOLO_PASS_X2, rN * A + NN8, N * fl * 2);
-        }
-        float2 *Gj = want_q ? p->G + (size_t)j * LL : nullptr;
-        float2 *T3j = gpsi ? p->T3 + (size_t)j * LL : nullptr;
-        TabSeq q2{};
-        q2.p[q2.n++] = p->hdet + (size_t)j * L;
-        if (T3j) {
-          if (mag)
-            add_adj(q2, k, j, 1);
-          else
-            q2.p[q2.n++] = crp(k, j, 1);
-        }
-        pbeg(p);
-        k_y2<L><<<L / G, NT, SM::XPT, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, tb, q2, mag, N);
-        pend(p, HOLO_PASS_Y2, rN * A + (Gj ? 3 * A : 0) + (T3j ? 2 * A : 0),
-             L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0)));
-      }
-      if (gpsi && (mode == 0 || mode == 2)) {
-        TabSeq q3{};
-        for (int j = 0; j < nz; j++) {
-          if ((p->magmask >> j) & 1u)
-            add_adj(q3, k, j, 0);
-          else
-            q3.p[q3.n++] = crp(k, j, 0);
-        }
-        pbeg(p);
-        k_x3<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T3, eta ? eta + (size_t)k * LL : nullptr, gpsi + (size_t)k * LL,
-                                                p->partX3 + (size_t)k * 2 * p->nbx3, tb, q3, nz, p->magmask, gscale);
-        pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
-      }
-    }
-    if (want_q && (mode == 0 || mode == 2)) gq(p, gq_out, gscale, false);
-  }
-};
-
-template <template <int> class R, class... A>
-void dispatch_sweep(holo_plan *p, A... a) {
-  switch (p->L) {
-    case 128: R<128>::sweep(p, a...); break;
-    case 256: R<256>::sweep(p, a...); break;
-    case 512: R<512>::sweep(p, a...); break;
-    case 1024: R<1024>::sweep(p, a...); break;
-    case 2048: R<2048>::sweep(p, a...); break;
-    case 4096: R<4096>::sweep(p, a...); break;
-  }
-}
-
 // spectrum factor per (k, j, axis): cr[f] = cin_j[f] r_s[f] for magnified planes, r_s[f] / L at mt = 1,
 // r_s[f] = e^{-2 pi i fbar s / L} (O4 / O5; the shift precedes the magnification, reading C4)
 holo_status upload_cr(holo_plan *p, const double *s) {
@@ -459,67 +161,6 @@ holo_status upload_cr(holo_plan *p, const double *s) {
   HC(cudaMemcpy(p->cr, r.data(), r.size() * sizeof(float2), cudaMemcpyHostToDevice));
   return HOLO_OK;
 }
-
-// ------------------------------------------------------------------ reference arm runner (O14)
-template <int L>
-struct RefRun {
-  using E = LineEng<L>;
-  // w[r] = C(P_{zeta0} S_{s_r} q), row-major [R][N][N]
-  static void fwd(holo_plan *p, const float2 *q, float2 *w) {
-    const int N = p->N, R = p->n_ref;
-    const size_t SM = E::SMEM;
-    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
-    const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
-    const double A = 8.0 * L * L, fl = fftf(L);
-    pbeg(p);
-    k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, p->tw3, N, 1.f, 0);
-    k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, p->tw3, N, 0);
-    pend(p, HOLO_PASS_REF, 4 * A, 2.0 * L * fl);
-    for (int r = 0; r < R; r++) {
-      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
-      pbeg(p);
-      k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, p->tw3, N, 0);
-      k_ref_rows<L, REF_FWD><<<gn, E::NT, SM, p->stream>>>(p->Wr, nullptr, w + (size_t)r * N * N, nullptr, Hx, tw,
-                                                             p->tw3, N, 1.f, 0);
-      pend(p, HOLO_PASS_REF, A * 2.0 + 8.0 * N * N, fl * (L + N));
-    }
-  }
-
-  static void run(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc) {
-    const int N = p->N, R = p->n_ref;
-    const size_t SM = E::SMEM;
-    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
-    const float2 *tw3 = p->tw3;
-    const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
-    const double A = 8.0 * L * L, fl = fftf(L);
-    // Qhat = DFT2(q)
-    pbeg(p);
-    k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, tw3, N, 1.f, 0);
-    k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, tw3, N, 0);
-    pend(p, HOLO_PASS_REF, 4 * A, 2.0 * L * fl);
-    for (int r = 0; r < R; r++) {
-      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
-      pbeg(p);
-      k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, tw3, N, 0);
-      k_ref_rows<L, REF_R2><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r * N * N, p->Vr,
-                                                            p->partR + (size_t)r * gn, Hx, tw, tw3, N, 1.f, 0,
-                                                            p->tau2);
-      if (gq) k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, tw3, N, r == 0);
-      pend(p, HOLO_PASS_REF, A * (1.0 + 0.5 + 0.5 + 1.0 / 8 + 0.5 + (gq ? 0.5 + (r ? 2.0 : 1.0) : 0.0)),
-           fl * (L + 2.0 * N + (gq ? L : 0)));
-    }
-    if (gq) {
-      pbeg(p);
-      k_ref_cols<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, p->Ghat, nullptr, tw, tw3, N, 0);
-      k_ref_rows<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, nullptr, gq, nullptr, nullptr, tw, tw3, N,
-                                                               2.0f, acc ? 1 : 0);
-      pend(p, HOLO_PASS_REF, (acc ? 5 : 4) * A, 2.0 * L * fl);
-    }
-    pbeg(p);
-    k_reduce<<<1, 1024, 0, p->stream>>>(p->partR, (size_t)R * gn, 1, sc, 0);
-    pend(p, HOLO_PASS_REDUCE, 8.0 * R * gn, 0);
-  }
-};
 
 holo_status precheck(holo_plan *p) {
   if (!p) return HOLO_EINVAL;
@@ -550,7 +191,12 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   if (!supported_L(L)) return HOLO_EUNSUPPORTED;
   if (!chain_L(L) && K > 0) return HOLO_EUNSUPPORTED;
   if (N % 4) return HOLO_EUNSUPPORTED;  // float4 row I/O of N-wide frames
+  if (g->angle_batch < 1 || g->angle_batch > HOLO_MAX_BATCH) return HOLO_EINVAL;
+  const HoloOps *ops = holo_ops_for(L);
+  if (!ops || (K > 0 && !ops->sweep)) return HOLO_EUNSUPPORTED;
   holo_plan *p = new holo_plan();
+  p->ops = ops;
+  p->B = g->angle_batch < (K > 0 ? K : 1) ? g->angle_batch : (K > 0 ? K : 1);
   p->device = device;
   p->stream = reinterpret_cast<cudaStream_t>(stream);
   p->g = *g;
@@ -567,11 +213,11 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
     if (p->mt[j] != 1.0) p->magmask |= 1u << j;
   }
   if (cudaSetDevice(device) != cudaSuccess) { delete p; return HOLO_ECUDA; }
-  set_attrs(L);
+  ops->set_attrs();
   holo_status s = HOLO_OK;
   const size_t LL = (size_t)L * L;
   auto A = [&](auto **ptr, size_t bytes) { if (s == HOLO_OK) s = dalloc(p, ptr, bytes); };
-  const int GR = 16 * NT / L;  // lines per CTA of the line kernels (CtaK<L>::G)
+  const int GR = 16 * 512 / L;  // lines per CTA of the object-chain line kernels (CtaK<L>::G, 512 threads)
   p->nbx2 = (N + GR - 1) / GR;
   p->nbx3 = L / GR;
   const size_t Kc = (size_t)(K > 0 ? K : 1);
@@ -582,17 +228,16 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   A(&p->hdet, sizeof(float2) * L * nz);
   A(&p->homega, sizeof(float2) * L * nz);
   A(&p->cout, sizeof(float2) * L * nz);
-  A(&p->cwo, sizeof(float2) * L * nz);
   A(&p->bke, sizeof(float2) * L * nz);
   A(&p->bko, sizeof(float2) * L * nz);
-  A(&p->wodd, sizeof(float2) * L);
   A(&p->cr, sizeof(float2) * L * 2 * nz * Kc);
   const size_t LLc = K > 0 ? LL : 0;  // object-chain workspace only when the plan holds angles
-  A(&p->T1, sizeof(float2) * LLc * nz);
-  A(&p->Aw, sizeof(float2) * LLc);
-  A(&p->W1, sizeof(float2) * (K > 0 ? (size_t)N * L : 0));
-  A(&p->V1, sizeof(float2) * (K > 0 ? (size_t)N * L : 0));
-  A(&p->T3, sizeof(float2) * LLc * nz);
+  const size_t Bc = (size_t)p->B;     // batch-sized per-frame workspace (holo_run.cuh)
+  A(&p->T1, sizeof(float2) * LLc * nz * Bc);
+  A(&p->Aw, sizeof(float2) * LLc * Bc);
+  A(&p->W1, sizeof(float2) * (K > 0 ? (size_t)N * L * Bc : 0));
+  A(&p->V1, sizeof(float2) * (K > 0 ? (size_t)N * L * Bc : 0));
+  A(&p->T3, sizeof(float2) * LLc * nz * Bc);
   A(&p->G, sizeof(float2) * LLc * nz);
   A(&p->QJ, sizeof(float2) * LLc * nz);
   A(&p->partF, sizeof(double) * Kc * nz * p->nbx2);
@@ -609,9 +254,7 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
         for (int e : {1, 2, 4, 8}) tw.push_back(expi2pi_frac(-(double)((long)m * e) / (16.0 * Ns)));
     if (tw.size() != 4 * twrows) { holo_plan_destroy(p); return HOLO_EUNSUPPORTED; }
     if (s == HOLO_OK) s = upload(p, p->tw, tw);
-    std::vector<cd> wo(L);
-    for (int i = 0; i < L; i++) wo[i] = expi2pi_frac(-(double)i / (2.0 * L));  // w[i] = e^{-i pi i / L}
-    std::vector<cd> hd, ho, co, cw, be, bo;
+    std::vector<cd> hd, ho, co, be, bo;
     p->cin_host.clear();
     if (!chain_L(L)) {  // radix-3 combine twiddles W_6144^{g k}, g = 1, 2 (holo_ref.cuh)
       std::vector<cd> t3;
@@ -639,7 +282,6 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
         long n = o - L / 2;
         cd c = expi2pi_frac(std::fmod(mt * (double)(n * n), 2.0 * L) / (2.0 * L));
         co.push_back(c);
-        cw.push_back(c * std::conj(wo[o]));
       }
       // b[d] = exp(-i pi mt d^2 / L), |d| < L, on a 2L cycle; Bhat = FFT_2L(b) / (2L)
       std::vector<cd> b(2 * L, cd(0, 0));
@@ -658,11 +300,9 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
       if (s == HOLO_OK) s = upload(p, p->hdet, hd);
       if (s == HOLO_OK) s = upload(p, p->homega, ho);
       if (s == HOLO_OK) s = upload(p, p->cout, co);
-      if (s == HOLO_OK) s = upload(p, p->cwo, cw);
       if (s == HOLO_OK) s = upload(p, p->bke, be);
       if (s == HOLO_OK) s = upload(p, p->bko, bo);
     }
-    if (s == HOLO_OK) s = upload(p, p->wodd, wo);
   }
   if (s == HOLO_OK && K > 0) {  // zero shifts until holo_set_shifts
     std::vector<double> zero((size_t)K * nz * 2, 0.0);
@@ -748,8 +388,13 @@ holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
     if (st == HOLO_OK) st = dalloc(p, &p->Vr, sizeof(float2) * (size_t)N * L);
     if (st != HOLO_OK) return st;
   }
-  if (n_ref > p->ref_cap) {
-    const int nbr = (N + 15) / 1;  // >= R2 CTAs per frame for every engine (G >= 1)
+  if (n_ref > p->ref_cap) {  // (re)size the per-frame tables; the old ones are freed, not leaked
+    const int G = p->ops->ref_lines_per_cta;
+    const int nbr = (N + G - 1) / G;  // CTAs of one frame's R2 row pass (one F partial each)
+    HC(cudaStreamSynchronize(p->stream));  // a queued reference sweep may still read them
+    dfree(p, (void **)&p->Href);
+    dfree(p, (void **)&p->partR);
+    p->ref_cap = 0;
     st = dalloc(p, &p->Href, sizeof(float2) * 2 * L * (size_t)n_ref);
     if (st == HOLO_OK) st = dalloc(p, &p->partR, sizeof(double) * (size_t)nbr * n_ref);
     if (st != HOLO_OK) return st;
@@ -776,8 +421,9 @@ holo_status holo_fwd(holo_plan *p, const void *psi, const void *q, void *w) {
   holo_status st = precheck(p);
   if (st != HOLO_OK) return st;
   if (!psi || !q || !w) return fail(p, HOLO_EINVAL, "null pointer");
-  dispatch_sweep<Run>(p, 1, (const float2 *)psi, (const float2 *)q, (const float *)nullptr, (const float2 *)nullptr,
-                      (float2 *)w, (const float2 *)nullptr, (float2 *)nullptr, (float2 *)nullptr, 1.0f, false);
+  if (p->K == 0) return HOLO_OK;
+  p->ops->sweep(p, 1, (const float2 *)psi, (const float2 *)q, nullptr, nullptr, (float2 *)w, nullptr, nullptr,
+                nullptr, 1.0f, false, false);
   return postcheck(p);
 }
 
@@ -786,9 +432,12 @@ holo_status holo_adj(holo_plan *p, const void *y, const void *psi, const void *q
   if (st != HOLO_OK) return st;
   if (!y || !psi || !q) return fail(p, HOLO_EINVAL, "null pointer");
   if (!adj_psi && !adj_q) return HOLO_OK;
-  dispatch_sweep<Run>(p, 2, (const float2 *)psi, (const float2 *)q, (const float *)nullptr, (const float2 *)y,
-                      (float2 *)nullptr, (const float2 *)nullptr, (float2 *)adj_psi, (float2 *)adj_q, 1.0f,
-                      adj_q != nullptr);
+  if (p->K == 0) {  // sums over no angles
+    if (adj_q) HC(cudaMemsetAsync(adj_q, 0, sizeof(float2) * (size_t)p->L * p->L, p->stream));
+    return HOLO_OK;
+  }
+  p->ops->sweep(p, 2, (const float2 *)psi, (const float2 *)q, nullptr, (const float2 *)y, nullptr, nullptr,
+                (float2 *)adj_psi, (float2 *)adj_q, 1.0f, adj_q != nullptr, false);
   return postcheck(p);
 }
 
@@ -798,17 +447,16 @@ holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float 
   if (st != HOLO_OK) return st;
   const int K = p->K, nz = p->nz, N = p->N, L = p->L;
   if (!q || !sc || (K > 0 && (!psi || !sqrt_d))) return fail(p, HOLO_EINVAL, "null pointer");
-  if (flags & HOLO_ACCUMULATE_Q) return fail(p, HOLO_EUNSUPPORTED, "HOLO_ACCUMULATE_Q not implemented for holo_grad");
-  const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0;
+  const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0, acc = (flags & HOLO_ACCUMULATE_Q) != 0;
   p->tau2 = (flags & HOLO_INTENSITY) ? 1 : 0;
   HC(cudaMemsetAsync(sc, 0, 3 * sizeof(double), p->stream));
   if (K == 0) {  // empty shard: F = 0 and a zero probe-gradient partial (sums over no angles)
-    if (!obj && grad_q_part) HC(cudaMemsetAsync(grad_q_part, 0, sizeof(float2) * (size_t)L * L, p->stream));
+    if (!obj && grad_q_part && !acc) HC(cudaMemsetAsync(grad_q_part, 0, sizeof(float2) * (size_t)L * L, p->stream));
     return HOLO_OK;
   }
-  dispatch_sweep<Run>(p, obj ? 3 : 0, (const float2 *)psi, (const float2 *)q, sqrt_d, (const float2 *)nullptr,
-                      (float2 *)nullptr, (const float2 *)eta_psi_prev, obj ? nullptr : (float2 *)grad_psi,
-                      obj ? nullptr : (float2 *)grad_q_part, 2.0f, !obj && grad_q_part != nullptr);
+  p->ops->sweep(p, obj ? 3 : 0, (const float2 *)psi, (const float2 *)q, sqrt_d, nullptr, nullptr,
+                (const float2 *)eta_psi_prev, obj ? nullptr : (float2 *)grad_psi,
+                obj ? nullptr : (float2 *)grad_q_part, 2.0f, !obj && grad_q_part != nullptr, acc);
   pbeg(p);
   k_reduce<<<1, 1024, 0, p->stream>>>(p->partF, (size_t)K * nz * p->nbx2, 1, sc, 0);
   pend(p, HOLO_PASS_REDUCE, 8.0 * K * nz * ((N + 3) / 4), 0);
@@ -833,15 +481,7 @@ holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref, v
     if (gq && !acc) HC(cudaMemsetAsync(gq, 0, sizeof(float2) * (size_t)p->L * p->L, p->stream));
     return HOLO_OK;
   }
-  switch (p->L) {
-    case 128: RefRun<128>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
-    case 256: RefRun<256>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
-    case 512: RefRun<512>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
-    case 1024: RefRun<1024>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
-    case 2048: RefRun<2048>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
-    case 4096: RefRun<4096>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
-    case 6144: RefRun<6144>::run(p, (const float2 *)q, sqrt_dref, gq, sc, acc); break;
-  }
+  p->ops->ref_run(p, (const float2 *)q, sqrt_dref, gq, sc, acc);
   return postcheck(p);
 }
 
@@ -850,15 +490,7 @@ holo_status holo_fwd_ref(holo_plan *p, const void *q, void *w) {
   if (st != HOLO_OK) return st;
   if (!q || (p->n_ref > 0 && !w)) return fail(p, HOLO_EINVAL, "null pointer");
   if (p->n_ref == 0) return HOLO_OK;
-  switch (p->L) {
-    case 128: RefRun<128>::fwd(p, (const float2 *)q, (float2 *)w); break;
-    case 256: RefRun<256>::fwd(p, (const float2 *)q, (float2 *)w); break;
-    case 512: RefRun<512>::fwd(p, (const float2 *)q, (float2 *)w); break;
-    case 1024: RefRun<1024>::fwd(p, (const float2 *)q, (float2 *)w); break;
-    case 2048: RefRun<2048>::fwd(p, (const float2 *)q, (float2 *)w); break;
-    case 4096: RefRun<4096>::fwd(p, (const float2 *)q, (float2 *)w); break;
-    case 6144: RefRun<6144>::fwd(p, (const float2 *)q, (float2 *)w); break;
-  }
+  p->ops->ref_fwd(p, (const float2 *)q, (float2 *)w);
   return postcheck(p);
 }
 

@@ -1,0 +1,312 @@
+// holo_run.cuh -- pass orchestration for one torus size L (instantiated by inst_<L>.cu).
+//
+// Object chain (holo_fwd / holo_adj / holo_grad), per batch of B angles (B = plan->B):
+//   X1 per angle (rows)  ->  for each plane j: Y1 (cols, batched), X2 (rows, batched),
+//   Y2 (cols, batched)   ->  X3 per angle (rows)
+// then, once per sweep, g_q = 2 sum_j P_{-omega_j} G_j (filters).  DESIGN.md "Pass schedule".
+// Reference arm (holo_grad_ref / holo_fwd_ref, O14): RefRun.
+#pragma once
+#include "holo_impl.cuh"
+#include "holo_passes.cuh"
+#include "holo_ref.cuh"
+
+namespace holo_run {
+using namespace holo;
+
+template <int L>
+struct Smem {
+  static constexpr size_t X = CtaK<L>::XBYTES;                          // exchange space only (filters)
+  static constexpr size_t XT = X + TabPipe<L>::BYTES;                    // + two table slots
+  static constexpr size_t XPT = X + CtaK<L>::PRIV + TabPipe<L>::BYTES;  // + one thread-private line
+};
+
+template <int L>
+void set_chain_attrs() {
+  using S = Smem<L>;
+  auto a = [](const void *f, size_t s) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s); };
+  a((const void *)k_x1<L>, S::XPT);
+  a((const void *)k_y1<L>, S::XPT);
+  a((const void *)k_x2<L, X2_GRAD>, S::XT);
+  a((const void *)k_x2<L, X2_FWD>, S::XT);
+  a((const void *)k_x2<L, X2_ADJ>, S::XT);
+  a((const void *)k_x2<L, X2_OBJ>, S::XT);
+  a((const void *)k_y2<L>, S::XPT);
+  a((const void *)k_x3<L>, S::XPT);
+  a((const void *)k_rows_filter<L, false, true, false>, S::X);
+  a((const void *)k_rows_filter<L, true, false, false>, S::X);
+  a((const void *)k_rows_filter<L, true, false, true>, S::X);
+  a((const void *)k_cols_filter<L>, S::X);
+}
+
+template <int L>
+void set_ref_attrs() {
+  const int sz = (int)LineEng<L>::SMEM;
+  auto a = [&](const void *f) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, sz); };
+  a((const void *)k_ref_cols<L, REF_QHAT>);
+  a((const void *)k_ref_cols<L, REF_R1>);
+  a((const void *)k_ref_cols<L, REF_R3>);
+  a((const void *)k_ref_cols<L, REF_FINAL>);
+  a((const void *)k_ref_rows<L, REF_QHAT>);
+  a((const void *)k_ref_rows<L, REF_R2>);
+  a((const void *)k_ref_rows<L, REF_FINAL>);
+  a((const void *)k_ref_rows<L, REF_FWD>);
+}
+
+// ------------------------------------------------------------------ object chain
+template <int L>
+struct Run {
+  using SM = Smem<L>;
+  static constexpr int G = CtaK<L>::G;
+  static constexpr double A = 8.0 * L * L;  // bytes of one L x L complex64 array
+
+  // q_j = P_{omega_j} q (O6): row-major q -> P2 QJ_j
+  static void qj(holo_plan *p, const float2 *q) {
+    const Tables tb = p->tables();
+    for (int j = 0; j < p->nz; j++) {
+      float2 *dst = p->QJ + (size_t)j * L * L;
+      pbeg(p);
+      if (p->omega[j] == 0.0) {
+        k_p2_convert<<<1184, 256, 0, p->stream>>>(q, dst, L, 1, 1.0f, 0);
+        pend(p, HOLO_PASS_FILTER, 2 * A, 0);
+        continue;
+      }
+      k_rows_filter<L, false, true, false><<<L / G, NT, SM::X, p->stream>>>(q, dst, tb, p->homega + j * L, 0, 1.0f);
+      k_cols_filter<L><<<L / G, NT, SM::X, p->stream>>>(dst, dst, tb, p->homega + j * L, 0, 1.0f);
+      pend(p, HOLO_PASS_FILTER, 4 * A, 4.0 * L * fftf(L), 2);
+    }
+  }
+
+  // g_q (+)= scale * sum_j P_{-omega_j} G_j   (G_j P2 -> row-major out)
+  static void gq(holo_plan *p, float2 *out, float scale, bool accumulate) {
+    const Tables tb = p->tables();
+    for (int j = 0; j < p->nz; j++) {
+      float2 *Gj = p->G + (size_t)j * L * L;
+      const bool acc = accumulate || j > 0;
+      pbeg(p);
+      if (p->omega[j] == 0.0) {
+        k_p2_convert<<<1184, 256, 0, p->stream>>>(Gj, out, L, 0, scale, acc ? 1 : 0);
+        pend(p, HOLO_PASS_FILTER, (acc ? 3 : 2) * A, 0);
+        continue;
+      }
+      k_cols_filter<L><<<L / G, NT, SM::X, p->stream>>>(Gj, Gj, tb, p->homega + j * L, 1, 1.0f);
+      if (acc)
+        k_rows_filter<L, true, false, true><<<L / G, NT, SM::X, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale);
+      else
+        k_rows_filter<L, true, false, false><<<L / G, NT, SM::X, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale);
+      pend(p, HOLO_PASS_FILTER, (acc ? 5 : 4) * A, 4.0 * L * fftf(L), 2);
+    }
+  }
+
+  // mode: 0 grad, 1 fwd, 2 adj (y given), 3 objective only
+  static void sweep(holo_plan *p, int mode, const float2 *psi, const float2 *q, const float *sqrt_d,
+                    const float2 *yin, float2 *wout, const float2 *eta, float2 *gpsi, float2 *gq_out, float gscale,
+                    bool want_q, bool acc_q) {
+    Tables tb = p->tables();
+    const int N = p->N, nz = p->nz, K = p->K;
+    const size_t LL = (size_t)L * L, NL = (size_t)N * L, NN = (size_t)N * N;
+    const int nbx2 = p->nbx2;
+    const double fl = fftf(L), rN = (double)N / L, NN8 = 8.0 * N * N;
+    int nmag = 0;
+    for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
+    qj(p, q);
+    if (want_q) cudaMemsetAsync(p->G, 0, sizeof(float2) * LL * nz, p->stream);
+    // table sequences of the pipelined pointwise steps (holo_kernels.cuh, TabPipe)
+    auto crp = [&](int k, int j, int ax) { return p->cr + ((size_t)(k * nz + j) * 2 + ax) * L; };
+    auto add_fwd = [&](TabSeq &q, int k, int j, int ax) {  // mag_fwd: cr, bke, cr, bko, cout
+      const float2 *c = crp(k, j, ax);
+      const float2 *list[5] = {c, p->bke + (size_t)j * L, c, p->bko + (size_t)j * L, p->cout + (size_t)j * L};
+      for (auto *e : list) q.p[q.n++] = e;
+    };
+    auto add_adj = [&](TabSeq &q, int k, int j, int ax) {  // mag_adj: cout, bke, cout, bko, cr
+      const float2 *c = p->cout + (size_t)j * L;
+      const float2 *list[5] = {c, p->bke + (size_t)j * L, c, p->bko + (size_t)j * L, crp(k, j, ax)};
+      for (auto *e : list) q.p[q.n++] = e;
+    };
+    const bool need_fwd_chain = (mode != 2) || want_q;
+    for (int k0 = 0; k0 < K; k0 += p->B) {
+      const int nb = K - k0 < p->B ? K - k0 : p->B;  // ragged last batch
+      // ---- X1 (per angle): T1[b][j] = (M S)_x psi_k rows
+      if (need_fwd_chain) {
+        for (int b = 0; b < nb; b++) {
+          const int k = k0 + b;
+          TabSeq q{};
+          for (int j = 0; j < nz; j++) {
+            if ((p->magmask >> j) & 1u)
+              add_fwd(q, k, j, 0);
+            else
+              q.p[q.n++] = crp(k, j, 0);
+          }
+          pbeg(p);
+          k_x1<L><<<L / G, NT, SM::XPT, p->stream>>>(psi + (size_t)k * LL, p->T1 + (size_t)b * nz * LL, tb, q, nz,
+                                                      p->magmask);
+          pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * (1 + 4 * nmag + (nz - nmag)));
+        }
+      }
+      for (int j = 0; j < nz; j++) {
+        const int mag = (p->magmask >> j) & 1;
+        const float2 *qjj = p->QJ + (size_t)j * LL;
+        // ---- Y1 (batched): Aw[b] = (M S)_y T1[b][j];  W1[b] = crop_y D_y (q_j Aw[b])
+        if (need_fwd_chain) {
+          float2 *aout = want_q ? p->Aw : nullptr;
+          float2 *w1 = (mode == 2) ? nullptr : p->W1;
+          TabSeq q{};
+          for (int b = 0; b < nb; b++) {
+            if (mag)
+              add_fwd(q, k0 + b, j, 1);
+            else
+              q.p[q.n++] = crp(k0 + b, j, 1);
+            if (w1) q.p[q.n++] = p->hdet + (size_t)j * L;
+          }
+          pbeg(p);
+          k_y1<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T1 + (size_t)j * LL, (size_t)nz * LL, qjj, aout, w1, tb, q,
+                                                      mag, N, nb);
+          // bytes: T1 read, Aw write, W1 write per frame; q_j once per batch (L2-resident)
+          pend(p, HOLO_PASS_Y1, nb * (A + (w1 ? rN * A : 0) + (aout ? A : 0)) + (w1 ? A : 0),
+               nb * L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0)));
+        }
+        // ---- X2 (batched over blockIdx.y)
+        double *pf = p->partF + ((size_t)k0 * nz + j) * nbx2;
+        TabSeq qh{};
+        qh.p[qh.n++] = p->hdet + (size_t)j * L;
+        if (mode == 0 || mode == 2) qh.p[qh.n++] = p->hdet + (size_t)j * L;
+        const dim3 g2(nbx2, nb);
+        const size_t fo = (size_t)k0 * nz + j;  // first frame of the batch in [k][j] order
+        pbeg(p);
+        if (mode == 1) {
+          k_x2<L, X2_FWD><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, nullptr, 0, wout + fo * NN, nz * NN, pf,
+                                                         nz * nbx2, tb, qh, N, p->tau2);
+          pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
+          continue;
+        }
+        if (mode == 3) {
+          k_x2<L, X2_OBJ><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, sqrt_d + fo * NN, nz * NN, nullptr, 0, pf,
+                                                         nz * nbx2, tb, qh, N, p->tau2);
+          pend(p, HOLO_PASS_X2, nb * (rN * A + NN8 / 2), nb * N * fl * 2);
+          continue;
+        }
+        if (mode == 0) {
+          k_x2<L, X2_GRAD><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, sqrt_d + fo * NN, nz * NN, p->V1, NL, pf,
+                                                          nz * nbx2, tb, qh, N, p->tau2);
+          pend(p, HOLO_PASS_X2, nb * (2 * rN * A + NN8 / 2), nb * N * fl * 4);
+        } else {
+          k_x2<L, X2_ADJ><<<g2, NT, SM::XT, p->stream>>>(yin + fo * NN, nz * NN, nullptr, 0, p->V1, NL, pf,
+                                                         nz * nbx2, tb, qh, N, p->tau2);
+          pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
+        }
+        // ---- Y2 (batched): v = D_y^* V1[b]; G_j += conj(Aw[b]) v; T3[b][j] = (M S)_y^* (conj(q_j) v)
+        float2 *Gj = want_q ? p->G + (size_t)j * LL : nullptr;
+        float2 *T3j = gpsi ? p->T3 + (size_t)j * LL : nullptr;
+        TabSeq q2{};
+        for (int b = 0; b < nb; b++) {
+          q2.p[q2.n++] = p->hdet + (size_t)j * L;
+          if (T3j) {
+            if (mag)
+              add_adj(q2, k0 + b, j, 1);
+            else
+              q2.p[q2.n++] = crp(k0 + b, j, 1);
+          }
+        }
+        pbeg(p);
+        k_y2<L><<<L / G, NT, SM::XPT, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, (size_t)nz * LL, tb, q2, mag, N, nb);
+        // bytes: V1 read, Aw read (G_j), T3 write per frame; G_j read + write and q_j once per batch
+        pend(p, HOLO_PASS_Y2, nb * (rN * A + (Gj ? A : 0) + (T3j ? A : 0)) + (Gj ? 2 * A : 0) + (T3j ? A : 0),
+             nb * L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0)));
+      }
+      // ---- X3 (per angle): g_k = 2 IFFT_x( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3[b][j]
+      if (gpsi && (mode == 0 || mode == 2)) {
+        for (int b = 0; b < nb; b++) {
+          const int k = k0 + b;
+          TabSeq q3{};
+          for (int j = 0; j < nz; j++) {
+            if ((p->magmask >> j) & 1u)
+              add_adj(q3, k, j, 0);
+            else
+              q3.p[q3.n++] = crp(k, j, 0);
+          }
+          pbeg(p);
+          k_x3<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T3 + (size_t)b * nz * LL, eta ? eta + (size_t)k * LL : nullptr,
+                                                      gpsi + (size_t)k * LL, p->partX3 + (size_t)k * 2 * p->nbx3, tb,
+                                                      q3, nz, p->magmask, gscale);
+          pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
+        }
+      }
+    }
+    if (want_q && (mode == 0 || mode == 2)) gq(p, gq_out, gscale, acc_q);
+  }
+};
+
+// ------------------------------------------------------------------ reference arm runner (O14)
+template <int L>
+struct RefRun {
+  using E = LineEng<L>;
+  // w[r] = C(P_{zeta0} S_{s_r} q), row-major [R][N][N]
+  static void fwd(holo_plan *p, const float2 *q, float2 *w) {
+    const int N = p->N, R = p->n_ref;
+    const size_t SM = E::SMEM;
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
+    const double A = 8.0 * L * L, fl = fftf(L);
+    pbeg(p);
+    k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, p->tw3, N, 1.f, 0);
+    k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, p->tw3, N, 0);
+    pend(p, HOLO_PASS_REF, 4 * A, 2.0 * L * fl, 2);
+    for (int r = 0; r < R; r++) {
+      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
+      pbeg(p);
+      k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, p->tw3, N, 0);
+      k_ref_rows<L, REF_FWD><<<gn, E::NT, SM, p->stream>>>(p->Wr, nullptr, w + (size_t)r * N * N, nullptr, Hx, tw,
+                                                             p->tw3, N, 1.f, 0);
+      pend(p, HOLO_PASS_REF, A * 2.0 + 8.0 * N * N, fl * (L + N), 2);
+    }
+  }
+
+  static void run(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc) {
+    const int N = p->N, R = p->n_ref;
+    const size_t SM = E::SMEM;
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const float2 *tw3 = p->tw3;
+    const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
+    const double A = 8.0 * L * L, fl = fftf(L);
+    // Qhat = DFT2(q)
+    pbeg(p);
+    k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, tw3, N, 1.f, 0);
+    k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, tw3, N, 0);
+    pend(p, HOLO_PASS_REF, 4 * A, 2.0 * L * fl, 2);
+    for (int r = 0; r < R; r++) {
+      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
+      pbeg(p);
+      k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, tw3, N, 0);
+      k_ref_rows<L, REF_R2><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r * N * N, p->Vr,
+                                                            p->partR + (size_t)r * gn, Hx, tw, tw3, N, 1.f, 0,
+                                                            p->tau2);
+      if (gq) k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, tw3, N, r == 0);
+      pend(p, HOLO_PASS_REF, A * (1.0 + 0.5 + 0.5 + 1.0 / 8 + 0.5 + (gq ? 0.5 + (r ? 2.0 : 1.0) : 0.0)),
+           fl * (L + 2.0 * N + (gq ? L : 0)), gq ? 3 : 2);
+    }
+    if (gq) {
+      pbeg(p);
+      k_ref_cols<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, p->Ghat, nullptr, tw, tw3, N, 0);
+      k_ref_rows<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, nullptr, gq, nullptr, nullptr, tw, tw3, N,
+                                                               2.0f, acc ? 1 : 0);
+      pend(p, HOLO_PASS_REF, (acc ? 5 : 4) * A, 2.0 * L * fl, 2);
+    }
+    pbeg(p);
+    k_reduce<<<1, 1024, 0, p->stream>>>(p->partR, (size_t)R * gn, 1, sc, 0);
+    pend(p, HOLO_PASS_REDUCE, 8.0 * R * gn, 0);
+  }
+};
+
+}  // namespace holo_run
+
+// One HoloOps per L (object chain + reference arm), and the reference-arm-only size (6144).
+#define HOLO_DEFINE_OPS(LV)                                                                                      \
+  static void holo_set_attrs_##LV() {                                                                           \
+    holo_run::set_ref_attrs<LV>();                                                                              \
+    holo_run::set_chain_attrs<LV>();                                                                            \
+  }                                                                                                             \
+  extern const HoloOps holo_ops_##LV = {LV, holo_set_attrs_##LV, holo_run::Run<LV>::sweep,                      \
+                                        holo_run::RefRun<LV>::run, holo_run::RefRun<LV>::fwd, holo::LineEng<LV>::G};
+#define HOLO_DEFINE_REF_OPS(LV)                                                                                  \
+  static void holo_set_attrs_##LV() { holo_run::set_ref_attrs<LV>(); }                                          \
+  extern const HoloOps holo_ops_##LV = {LV, holo_set_attrs_##LV, nullptr, holo_run::RefRun<LV>::run,            \
+                                        holo_run::RefRun<LV>::fwd, holo::LineEng<LV>::G};

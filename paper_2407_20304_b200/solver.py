@@ -58,12 +58,11 @@ class JointCG:
         """F and grad at (psi, q); returns host (F, gg_psi, geta_psi, gg_q, geta_q)."""
         p = self.plan
         sc3 = self.sc[:3]
-        if p.K > 0:
-            p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
-        else:
-            sc3.zero_()
+        # always called, also on a rank without angles: holo_grad then writes F = 0 and a ZERO
+        # probe-gradient partial, so no stale (already reduced) g_q enters the allreduce
+        p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
         if self.dref is not None:  # reference arm: F_ref into sc[0], its gradient added to g_q
-            p.grad_ref(q, self.dref, self.scr, g_q, flags=HOLO_ACCUMULATE_Q if p.K > 0 else 0)
+            p.grad_ref(q, self.dref, self.scr, g_q, flags=HOLO_ACCUMULATE_Q)
             sc3[:1] += self.scr
         if self.dist:
             # exchange 1: probe-gradient partial (complex64 viewed as float32), exchange 2: scalars

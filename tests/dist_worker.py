@@ -29,6 +29,11 @@ class FakePlan:
         self.K = shifts.shape[0]
 
     def grad(self, psi, q, sqrt_d, sc, eta_psi_prev=None, grad_psi=None, grad_q_part=None, flags=0):
+        if self.K == 0:  # holo_grad on an empty shard: F = 0, zero probe-gradient partial
+            sc.zero_()
+            if grad_q_part is not None and not flags & 1:
+                grad_q_part.zero_()
+            return
         F, gp, gq = oracle.grad(self.g, psi.numpy(), q.numpy(), self.s, sqrt_d.numpy())
         sc[0] = F
         sc[1] = float(np.vdot(gp, gp).real)

@@ -38,17 +38,20 @@ def run(name, iters, world, tmp):
     return [np.load(o) for o in outs]
 
 
-@pytest.mark.parametrize("name,iters", [("joint", 3), ("ref", 4)])
-def test_two_ranks_match_one_process(name, iters, tmp_path):
+@pytest.mark.parametrize("name,iters,world", [("joint", 3, 2), ("ref", 4, 2), ("joint", 3, 5)])
+def test_two_ranks_match_one_process(name, iters, world, tmp_path):
+    """world = 5 > K = 4 angles: one rank holds an EMPTY shard and must contribute a zero
+    probe-gradient partial (not its stale, already reduced g_q) to the allreduce."""
     one = run(name, iters, 1, str(tmp_path))[0]
-    two = run(name, iters, 2, str(tmp_path))
+    two = run(name, iters, world, str(tmp_path))
     # every rank holds the identical q (replicated update, no broadcast)
-    assert np.array_equal(two[0]["q"], two[1]["q"])
+    for r in two[1:]:
+        assert np.array_equal(two[0]["q"], r["q"])
     for r in two:
         assert np.allclose(r["F"], one["F"], rtol=1e-10, atol=0)
         assert np.array_equal(r["gamma"], one["gamma"])
         assert np.linalg.norm(r["q"] - one["q"]) / np.linalg.norm(one["q"]) < 1e-10
     assert one["F"][-1] < one["F"][0]  # the iteration made progress
     if name == "joint":  # psi shards reassemble the single-process psi
-        psi2 = np.concatenate([two[0]["psi"], two[1]["psi"]])
+        psi2 = np.concatenate([r["psi"] for r in two])
         assert np.linalg.norm(psi2 - one["psi"]) / np.linalg.norm(one["psi"]) < 1e-10

@@ -26,11 +26,11 @@ def geom(cfg, z1=None):
     return oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1 if z1 is None else z1, cfg.det_pixel)
 
 
-def make_plan(cfg, K, L=None, N=None, z1=None):
+def make_plan(cfg, K, L=None, N=None, z1=None, batch=None):
     import paper_2407_20304_b200 as hb
     z1 = cfg.z1 if z1 is None else z1
     return hb.Plan(cfg.n if N is None else N, cfg.npad if L is None else L, z1, K, cfg.wavelength, cfg.Z,
-                   cfg.det_pixel, device=0)
+                   cfg.det_pixel, device=0, angle_batch=batch)
 
 
 def dev(x, dt=torch.complex64):
@@ -72,6 +72,17 @@ class Case:
         return npo.Problem(self.g, self.cfg.npad, self.cfg.n).grad(self.psi, self.q, self.s, self.d)
 
 
+def correlated_eta(g, seed=1):
+    """eta = -g e^{i phi} (1 + 0.2 n), phi a smooth random phase field in [-0.6, 0.6] rad: a
+    descent-like direction near -g (no cancellation in Re<g, eta>), as fp32."""
+    rng = np.random.default_rng(seed)
+    L = g.shape[-1]
+    yy, xx = np.meshgrid(np.arange(L), np.arange(L), indexing="ij")
+    phi = 0.6 * np.sin(2 * np.pi * (xx * rng.uniform(1, 3) + yy * rng.uniform(1, 3)) / L + rng.uniform(0, 6.3))
+    amp = 1 + 0.2 * rng.standard_normal(g.shape)
+    return (-g * np.exp(1j * phi) * amp).astype(np.complex64)
+
+
 @pytest.fixture(scope="module")
 def cfg0():
     return Case("cfg0", 4)
@@ -101,7 +112,9 @@ def test_cfg0_gradient_parity(cfg0):
     p.set_shifts(c.s)
     F, gp, gq = c.oracle_grad()
     assert np.linalg.norm(np.abs(oracle.fwd(c.g, c.psi, c.q, c.s, c.cfg.n)) - c.d) / np.linalg.norm(c.d) > 0.05
-    eta = (np.random.default_rng(1).standard_normal(c.psi.shape) * (1 + 1j)).astype(np.complex64)
+    # a direction correlated with the gradient (eta = -g with a smooth phase error), as a CG
+    # direction is: Re<g, eta> is then a well-conditioned sum and is held to the DY tolerance
+    eta = correlated_eta(gp)
     sc = torch.zeros(3, dtype=torch.float64, device="cuda")
     gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
     gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
@@ -111,8 +124,8 @@ def test_cfg0_gradient_parity(cfg0):
     assert rel(host(gpsi), gp) < TOL_G
     assert rel(host(gqd), gq) < TOL_G
     assert abs(s[1] - np.vdot(gp, gp).real) / np.vdot(gp, gp).real < TOL_S
-    ge = np.vdot(eta, gp).real
-    assert abs(s[2] - ge) / abs(ge) < 1e-3  # Re<g, eta> of random eta is a cancelling sum
+    ge = np.vdot(eta.astype(np.complex128), gp).real
+    assert abs(s[2] - ge) / abs(ge) < TOL_S
 
 
 def test_cfg0_objective_only_matches(cfg0):
@@ -195,9 +208,51 @@ def test_full_size_one_angle_parity(name):
     sc = torch.zeros(3, dtype=torch.float64, device="cuda")
     gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
     gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
-    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, gpsi, gqd)
-    assert abs(host(sc).real[0] - F) / F < TOL_S
+    eta = correlated_eta(gp, seed=3)
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, dev(eta), gpsi, gqd)
+    s = host(sc).real
+    assert abs(s[0] - F) / F < TOL_S
     assert rel(host(gpsi), gp) < TOL_G and rel(host(gqd), gq) < TOL_G
+    assert abs(s[1] - np.vdot(gp, gp).real) / np.vdot(gp, gp).real < TOL_S
+    ge = np.vdot(eta.astype(np.complex128), gp).real
+    assert abs(s[2] - ge) / abs(ge) < TOL_S
+
+
+@pytest.mark.parametrize("batch", [1, 4, 8])
+def test_angle_batch_ragged_parity(batch):
+    """angle_batch B in {1, 4, 8} on K = 6 angles of cfg1 (4 + 2 ragged for B = 4; B = 8 > K):
+    F, grad_psi, grad_q and the fused scalars vs the numpy oracle; also through holo_fwd."""
+    c = Case("cfg1", 6, oracle_kind="np")
+    p = make_plan(c.cfg, c.K, batch=batch)
+    p.set_shifts(c.s)
+    w = torch.empty(c.K, c.cfg.nz, c.cfg.n, c.cfg.n, dtype=torch.complex64, device="cuda")
+    p.fwd(dev(c.psi_t), dev(c.q_t), w)
+    assert rel(host(w), c.w) < TOL_W
+    F, gp, gq = c.oracle_grad()
+    eta = correlated_eta(gp, seed=batch)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, dev(eta), gpsi, gqd)
+    s = host(sc).real
+    assert abs(s[0] - F) / F < TOL_S
+    assert rel(host(gpsi), gp) < TOL_G and rel(host(gqd), gq) < TOL_G
+    ge = np.vdot(eta.astype(np.complex128), gp).real
+    assert abs(s[2] - ge) / abs(ge) < TOL_S
+
+
+def test_accumulate_q_flag(cfg0):
+    """HOLO_ACCUMULATE_Q adds the probe-gradient partial into grad_q_part (SURVEY 8b flag)."""
+    import paper_2407_20304_b200 as hb
+    c = cfg0
+    p = make_plan(c.cfg, c.K)
+    p.set_shifts(c.s)
+    F, gp, gq = c.oracle_grad()
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    base = (np.random.default_rng(4).standard_normal(c.q.shape) * (1 + 1j)).astype(np.complex64) * 1e-3
+    gqd = dev(base)
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, None, gqd, flags=hb.HOLO_ACCUMULATE_Q)
+    assert rel(host(gqd), gq + base) < TOL_G
 
 
 @pytest.mark.parametrize("name,K", [("cfg0", 4), ("cfg1", 2)])

@@ -14,7 +14,7 @@ UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 PASS = {"k_x1": "X1", "k_y1": "Y1", "k_x2": "X2", "k_y2": "Y2", "k_x3": "X3", "k_ref": "ref"}
 
 
-def main(rep, out):
+def main(rep, out, workload="cfg3", batch=8):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     head, units = rows[0], rows[1]
@@ -30,9 +30,12 @@ def main(rep, out):
     res = {k: sum(v) / len(v) for k, v in acc.items()}
     res["_launches"] = {k: len(v) for k, v in acc.items()}
     res["_source"] = rep
+    res["_workload"] = workload  # bench.py uses these per-launch bytes only for the same workload
+    res["_angle_batch"] = int(batch)
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "profiles/traffic.json")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "profiles/traffic.json",
+         sys.argv[3] if len(sys.argv) > 3 else "cfg3", sys.argv[4] if len(sys.argv) > 4 else 8)
