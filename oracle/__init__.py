@@ -63,6 +63,8 @@ def _load():
         lib.or_grad.restype = D
         lib.or_grad_ref.argtypes = [Ic, Ic, Ic, D, D, D, P, P, P, P]
         lib.or_grad_ref.restype = D
+        lib.or_upsample2.argtypes = [Ic, P, P]
+        lib.or_bin2.argtypes = [Ic, Ic, P, P]
         _lib = lib
     return _lib
 
@@ -203,4 +205,24 @@ def zpad(x, L):
     o = (L - N) // 2
     out = np.zeros(x.shape[:-2] + (L, L), dtype=np.result_type(x, np.complex128))
     out[..., o:o + N, o:o + N] = x
+    return out
+
+
+def upsample2(x):
+    """O15: Fourier 2x upsampling [L][L] -> [2L][2L], coarse sample n at fine coordinate
+    2n + 1/2 (multiresolution schedule P:258-259; reading R1).  Naive sums."""
+    x = _c(x, np.complex128)
+    L = x.shape[-1]
+    out = np.empty((2 * L, 2 * L), np.complex128)
+    _load().or_upsample2(L, _p(x), _p(out))
+    return out
+
+
+def bin2(a):
+    """O16: 2x2 binning of amplitudes a = sqrt(d~) [M][2N][2N] -> [M][N][N]: the binned
+    intensity is the block mean of the four intensities (reading R2)."""
+    a = _c(a, np.float64)
+    M, N = a.shape[0], a.shape[-1] // 2
+    out = np.empty((M, N, N), np.float64)
+    _load().or_bin2(M, N, _p(a), _p(out))
     return out

@@ -398,3 +398,62 @@ double or_grad_ref(int R, int L, int N, double lam, double p0, double zeta0,
   free(t); free(w);
   return F;
 }
+
+/* ------------------------------------------------------------------ O15 --- */
+/* Fourier 2x upsampling of an [L][L] field to [2L][2L] between levels of the
+ * multiresolution schedule ("extrapolate the recovered object with the probe
+ * function to a grid twice as dense").  Reading R1: the trigonometric
+ * interpolant of x, band fbar in [-L/2, L/2) (Nyquist bin at -L/2, reading C2), sampled at
+ * half-pixel steps with coarse sample n at fine coordinate 2n + 1/2 (the centre of the fine
+ * pixels a 2x2 bin merges, O16):
+ *   y[m] = (1/L) sum_f X[f] exp(+2 pi i fbar (m - 1/2) / (2L)),  X = DFT_L(x),  m in [0, 2L)
+ * applied along x (rows) then along y (columns).  Naive sums, no FFT.                  */
+static void up_line(long L, const cplx *W, const cplx *x, cplx *y, cplx *X) {
+  dft_line(L, 0, W, x, X);
+  for (long m = 0; m < 2 * L; m++) {
+    cplx acc = 0;
+    for (long f = 0; f < L; f++) acc += X[f] * cexp(2.0 * PI * I * (double)fbar_of(f, L) * ((double)m - 0.5) / (2.0 * L));
+    y[m] = acc / (double)L;
+  }
+}
+
+void or_upsample2(int L, const cplx *in, cplx *out) {
+  const long L2 = 2L * L;
+  cplx *W = twiddles(L);
+  cplx *mid = (cplx *)malloc(sizeof(cplx) * L * L2); /* [L][2L]: rows done */
+#pragma omp parallel
+  {
+    cplx *li = (cplx *)malloc(sizeof(cplx) * L), *lo = (cplx *)malloc(sizeof(cplx) * L2),
+         *X = (cplx *)malloc(sizeof(cplx) * L);
+#pragma omp for schedule(static)
+    for (long y = 0; y < L; y++) up_line(L, W, in + y * L, mid + y * L2, X);
+#pragma omp for schedule(static)
+    for (long x = 0; x < L2; x++) {
+      for (long y = 0; y < L; y++) li[y] = mid[y * L2 + x];
+      up_line(L, W, li, lo, X);
+      for (long m = 0; m < L2; m++) out[m * L2 + x] = lo[m];
+    }
+    free(li); free(lo); free(X);
+  }
+  free(mid); free(W);
+}
+
+/* ------------------------------------------------------------------ O16 --- */
+/* 2x2 binning of the measured amplitudes a = sqrt(d~) ("binning 8x8 ... 4x4"): the
+ * intensity of a binned pixel is the block MEAN of the four intensities (reading R2, the
+ * per-pixel intensity unit is kept; the detector pixel doubles), so
+ *   a_c[i][l] = sqrt( (1/4) sum_{a,b in {0,1}} a_f[2i+a][2l+b]^2 ),  count frames of [2N][2N]. */
+void or_bin2(int count, int N, const double *fine, double *coarse) {
+  const long N2 = 2L * N;
+  for (long c = 0; c < count; c++)
+    for (long i = 0; i < N; i++)
+      for (long l = 0; l < N; l++) {
+        double s = 0;
+        for (int a = 0; a < 2; a++)
+          for (int b = 0; b < 2; b++) {
+            const double v = fine[c * N2 * N2 + (2 * i + a) * N2 + 2 * l + b];
+            s += v * v;
+          }
+        coarse[c * (long)N * N + i * N + l] = sqrt(0.25 * s);
+      }
+}

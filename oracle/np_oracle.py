@@ -189,3 +189,23 @@ def grad_ref(wavelength, p0, zeta0, q, ref_shifts, sqrt_dref, want_q=True, tau=1
         if want_q:
             gq += 2.0 * shift(prop(zpad(rho, L), wavelength, p0, -zeta0), -sx, -sy)
     return F, gq
+
+
+def upsample2(x):
+    """O15 with numpy.fft as the DFT: per axis Y[F] = 2 X[F] e^{-i pi Fbar/(2L)} on the 2L grid for
+    Fbar in [-L/2, L/2) (zero elsewhere), y = IFFT_2L(Y)  (coarse n at fine 2n + 1/2, reading R1)."""
+    def last_axis(a):
+        L = a.shape[-1]
+        fbv = fbar(L)
+        Y = np.zeros(a.shape[:-1] + (2 * L,), np.complex128)
+        Y[..., np.where(fbv >= 0, fbv, fbv + 2 * L)] = np.fft.fft(a, axis=-1) * 2.0 * np.exp(-1j * np.pi * fbv / (2 * L))
+        return np.fft.ifft(Y, axis=-1)
+    y = last_axis(np.asarray(x, np.complex128))  # x (rows)
+    return last_axis(y.swapaxes(-1, -2)).swapaxes(-1, -2)  # then y (columns)
+
+
+def bin2(a):
+    """O16: a_c = sqrt(block mean of a^2) over 2x2 blocks, [..., 2N, 2N] -> [..., N, N]."""
+    a = np.asarray(a, np.float64)
+    s = a[..., 0::2, 0::2] ** 2 + a[..., 1::2, 0::2] ** 2 + a[..., 0::2, 1::2] ** 2 + a[..., 1::2, 1::2] ** 2
+    return np.sqrt(0.25 * s)
