@@ -471,7 +471,7 @@ def main():
                  "share_of_step": P["ms"] / ms_prof})
     # step level: T_roof = frames x max(B_min / BW, F_alg / P_FP32) against the measured step
     f_alg = sum(passes[k].get("flops_per_frame", 0) for k in chain)
-    t_frame = (ms / 1e3) / (frames * max(accepted, 1) / max(args.steps, 1)) if frames else None
+    t_frame = (ms / 1e3) / (frames * max(accepted, 1)) if frames else None  # ms spans all timed steps
     step = None
     if frames and f_alg:
         t_roof = max(B_MIN_A * A / (bw * 1e9), f_alg / (p32 * 1e12))

@@ -162,6 +162,18 @@ holo_status holo_cg_step(holo_plan *p, const holo_cg_in *in /*[host]*/, holo_cg_
                          const void *psi, void *eta_psi, const void *grad_psi, void *psi_trial,
                          const void *q, void *eta_q, const void *grad_q, void *q_trial);
 
+/* Multiresolution schedule ("binning 8x8 ... 4x4 ... then extrapolate
+ * the recovered object with the probe function to a grid twice as dense").
+ * holo_upsample2: Fourier 2x upsampling (O15, reading R1) of `count` complex64 fields
+ *   coarse [count][npad/2][npad/2] -> fine [count][npad][npad] (row-major, this plan = the FINE
+ *   level; npad a power of two).  Per axis y[m] = (1/L) sum_f X[f] e^{2 pi i fbar (m - 1/2)/(2L)},
+ *   L = npad/2, fbar in [-L/2, L/2): coarse sample n sits at fine coordinate 2n + 1/2.
+ *   Uses the plan's scratch; coarse and fine must not alias.  HOLO_EUNSUPPORTED for npad 6144.
+ * holo_bin2: 2x2 binning of amplitudes sqrt(d~) (O16, reading R2): fine [count][2n][2n] ->
+ *   coarse [count][n][n] (this plan = the COARSE level, n its data side), a_c = sqrt(mean a_f^2). */
+holo_status holo_upsample2(holo_plan *p, const void *coarse, void *fine, int32_t count);
+holo_status holo_bin2(holo_plan *p, const float *fine, float *coarse, int32_t count);
+
 /* Number of kernel launches this plan has enqueued since creation (profiling aid). */
 uint64_t holo_launch_count(const holo_plan *p);
 

@@ -82,6 +82,11 @@ _lib.holo_q_dots.restype = _S
 _lib.holo_cg_step.argtypes = [_P, ctypes.POINTER(HoloCgIn), ctypes.POINTER(HoloCgOut)] + [_P] * 8
 _lib.holo_cg_step.restype = _S
 
+_lib.holo_upsample2.argtypes = [_P, _P, _P, ctypes.c_int32]
+_lib.holo_upsample2.restype = _S
+_lib.holo_bin2.argtypes = [_P, _P, _P, ctypes.c_int32]
+_lib.holo_bin2.restype = _S
+
 _lib.holo_profile_enable.argtypes = [_P, ctypes.c_int]
 _lib.holo_profile_enable.restype = _S
 _lib.holo_profile_read.argtypes = [_P, _P, _P, _P, _P, ctypes.c_int]
@@ -95,7 +100,7 @@ PASS_KERNELS = ["k_x1", "k_y1", "k_x2", "k_y2", "k_x3", "k_rows_filter|k_cols_fi
 EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes", "holo_last_error",
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
             "holo_grad_ref", "holo_fwd_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
-            "holo_profile_read"]
+            "holo_profile_read", "holo_upsample2", "holo_bin2"]
 
 
 class HoloError(RuntimeError):
@@ -252,3 +257,19 @@ class Plan:
                                     _ptr(grad_q, torch.complex64, LL, "grad_q"),
                                     _ptr(q_trial, torch.complex64, LL, "q_trial")))
         return out
+
+    # ---- multiresolution schedule
+    def upsample2(self, coarse, fine):
+        """holo_upsample2: coarse [M][npad/2][npad/2] -> fine [M][npad][npad] (this plan = fine level)."""
+        Lc = self.npad // 2
+        M = coarse.numel() // (Lc * Lc)
+        self._chk(_lib.holo_upsample2(self._h, _ptr(coarse, torch.complex64, M * Lc * Lc, "coarse"),
+                                      _ptr(fine, torch.complex64, M * self.npad ** 2, "fine"), M))
+        return fine
+
+    def bin2(self, fine, coarse):
+        """holo_bin2: amplitudes fine [M][2n][2n] -> coarse [M][n][n] (this plan = coarse level)."""
+        M = coarse.numel() // (self.n * self.n)
+        self._chk(_lib.holo_bin2(self._h, _ptr(fine, torch.float32, M * 4 * self.n ** 2, "fine"),
+                                 _ptr(coarse, torch.float32, M * self.n ** 2, "coarse"), M))
+        return coarse

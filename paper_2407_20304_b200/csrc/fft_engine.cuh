@@ -126,6 +126,130 @@ __device__ __forceinline__ void dft_reg(float2 *v) {
   for (int i = 0; i < R; i++) v[i] = t[i];
 }
 
+// ---- radix-16 as a twiddle-absorbing DIT with FMA-fused butterflies (HOLO_DIT, default) ----
+// A twiddled radix-16 Stockham step computes y[k] = sum_s v[s] w^{ms} W16^{sk} = sum_s v[s] z_k^s,
+// z_k = omega W16^k (omega = w^m).  Radix-2 DIT on the bit-reversed register order: the level
+// with span H combines sub-DFTs with twiddles omega^{8/H} W_{2H}^k, k < H, so the four table
+// powers (omega, omega^2, omega^4, omega^8) plus 4 constant products are all the twiddles
+// needed, and every butterfly (a + t b, a - t b) costs 6 FP32 instructions (4 FFMA for
+// p = a + t b, then q = 2 a - p).  Per 16 points: 208 instructions for a twiddled stage and
+// 148 for the untwiddled first stage, against 272 / 168 for DIF + separate twiddle multiplies.
+#ifndef HOLO_DIT
+#define HOLO_DIT 1
+#endif
+
+// (a, b) <- (a + t b, a - t b), runtime twiddle t
+__device__ __forceinline__ void bfly(float2 &a, float2 &b, float2 t) {
+  float px = fmaf(t.x, b.x, a.x);
+  px = fmaf(-t.y, b.y, px);
+  float py = fmaf(t.x, b.y, a.y);
+  py = fmaf(t.y, b.x, py);
+  b = make_float2(fmaf(2.f, a.x, -px), fmaf(2.f, a.y, -py));
+  a = make_float2(px, py);
+}
+// (a, b) <- (a + t b, a - t b), t = W16^E (forward, e^{-2 pi i E/16}) or its conjugate (INV)
+template <int E, bool INV>
+__device__ __forceinline__ void bfly_c(float2 &a, float2 &b) {
+  if constexpr (E == 0) {
+    const float2 p = cadd(a, b);
+    b = csub(a, b);
+    a = p;
+  } else if constexpr (E == 4) {  // t = -i (fwd) / +i (inv)
+    const float2 tb = INV ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x);
+    const float2 p = cadd(a, tb);
+    b = csub(a, tb);
+    a = p;
+  } else {
+    constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f, H = 0.70710678118654752f;
+    constexpr float c = (E == 1) ? C1 : (E == 2) ? H : (E == 3) ? S1 : (E == 5) ? -S1 : (E == 6) ? -H : -C1;
+    constexpr float sn = (E == 1) ? S1 : (E == 2) ? H : (E == 3) ? C1 : (E == 5) ? C1 : (E == 6) ? H : S1;
+    bfly(a, b, make_float2(c, INV ? sn : -sn));
+  }
+}
+__host__ __device__ constexpr int brev4(int i) { return ((i & 1) << 3) | ((i & 2) << 1) | ((i & 4) >> 1) | ((i & 8) >> 3); }
+
+// untwiddled 16-point DFT, natural order in and out (first Stockham stage)
+template <bool INV>
+__device__ __forceinline__ void dft16_dit(float2 *v) {
+  float2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) a[i] = v[brev4(i)];
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) bfly_c<0, INV>(a[j], a[j + 1]);
+#pragma unroll
+  for (int j = 0; j < 16; j += 4) {
+    bfly_c<0, INV>(a[j], a[j + 2]);
+    bfly_c<4, INV>(a[j + 1], a[j + 3]);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; j += 8) {
+    bfly_c<0, INV>(a[j], a[j + 4]);
+    bfly_c<2, INV>(a[j + 1], a[j + 5]);
+    bfly_c<4, INV>(a[j + 2], a[j + 6]);
+    bfly_c<6, INV>(a[j + 3], a[j + 7]);
+  }
+  bfly_c<0, INV>(a[0], a[8]);
+  bfly_c<1, INV>(a[1], a[9]);
+  bfly_c<2, INV>(a[2], a[10]);
+  bfly_c<3, INV>(a[3], a[11]);
+  bfly_c<4, INV>(a[4], a[12]);
+  bfly_c<5, INV>(a[5], a[13]);
+  bfly_c<6, INV>(a[6], a[14]);
+  bfly_c<7, INV>(a[7], a[15]);
+#pragma unroll
+  for (int i = 0; i < 16; i++) v[i] = a[i];
+}
+
+// twiddled 16-point step: y[k] = sum_s v[s] (omega W16^k)^s, given omega^{1,2,4,8} (forward
+// convention; INV uses the conjugates)
+template <bool INV>
+__device__ __forceinline__ void dft16_dit_tw(float2 *v, float2 w1, float2 w2, float2 w4, float2 w8) {
+  constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f, H = 0.70710678118654752f;
+  auto mi = [](float2 z) { return make_float2(z.y, -z.x); };  // -i z
+  auto cj = [](float2 z) { return INV ? make_float2(z.x, -z.y) : z; };
+  // level twiddles (forward convention), then conjugated for INV
+  const float2 t0 = w1, t1 = make_float2(fmaf(w1.x, C1, w1.y * S1), fmaf(w1.y, C1, -w1.x * S1)),
+               t2 = make_float2((w1.x + w1.y) * H, (w1.y - w1.x) * H),
+               t3 = make_float2(fmaf(w1.x, S1, w1.y * C1), fmaf(w1.y, S1, -w1.x * C1));
+  const float2 s0 = w2, s1 = make_float2((w2.x + w2.y) * H, (w2.y - w2.x) * H);
+  float2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; i++) a[i] = v[brev4(i)];
+  {
+    const float2 t = cj(w8);
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) bfly(a[j], a[j + 1], t);
+  }
+  {
+    const float2 u0 = cj(w4), u1 = cj(mi(w4));
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      bfly(a[j], a[j + 2], u0);
+      bfly(a[j + 1], a[j + 3], u1);
+    }
+  }
+  {
+    const float2 q0 = cj(s0), q1 = cj(s1), q2 = cj(mi(s0)), q3 = cj(mi(s1));
+#pragma unroll
+    for (int j = 0; j < 16; j += 8) {
+      bfly(a[j], a[j + 4], q0);
+      bfly(a[j + 1], a[j + 5], q1);
+      bfly(a[j + 2], a[j + 6], q2);
+      bfly(a[j + 3], a[j + 7], q3);
+    }
+  }
+  bfly(a[0], a[8], cj(t0));
+  bfly(a[1], a[9], cj(t1));
+  bfly(a[2], a[10], cj(t2));
+  bfly(a[3], a[11], cj(t3));
+  bfly(a[4], a[12], cj(mi(t0)));
+  bfly(a[5], a[13], cj(mi(t1)));
+  bfly(a[6], a[14], cj(mi(t2)));
+  bfly(a[7], a[15], cj(mi(t3)));
+#pragma unroll
+  for (int i = 0; i < 16; i++) v[i] = a[i];
+}
+
 template <int L>
 struct Shape {
   static constexpr int LOG = ilog2c(L);
@@ -140,14 +264,36 @@ struct Shape {
   static_assert((1 << LOG) == L && L >= 128, "L must be a power of two >= 128");
 };
 
+// Line-local barrier (HOLO_LINE_BAR): with the thread-major CTA mapping (HOLO_TMAJOR) the
+// T threads of a line are whole warps (T >= 64: named barrier 1 + line, T threads) or live
+// inside one warp (T <= 32: __syncwarp), so the lines of a CTA synchronise independently and
+// one line's shared-memory exchange overlaps another line's butterflies.
+#ifndef HOLO_TMAJOR
+#define HOLO_TMAJOR 0
+#endif
+template <int T>
+__device__ __forceinline__ void line_sync(int g) {
+#if HOLO_TMAJOR
+  if constexpr (T <= 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(T) : "memory");
+  }
+#else
+  __syncthreads();
+#endif
+}
+
 // Exchange space of one line: two buffers of LP float2 at b and b + LPB.
 struct Xch {
   float2 *b;
   int par;
   int stride;
+  int g;  // line of this thread within the CTA (named barrier id - 1)
+  template <int T>
   __device__ __forceinline__ float2 *next() {
 #if HOLO_SINGLE_BUF
-    __syncthreads();  // previous readers of the single buffer are done
+    line_sync<T>(g);  // previous readers of the single buffer are done
     return b;
 #else
     float2 *p = par ? b + stride : b;
@@ -155,6 +301,8 @@ struct Xch {
     return p;
 #endif
   }
+  template <int T>
+  __device__ __forceinline__ void sync() { line_sync<T>(g); }
 };
 
 template <bool INV>
@@ -166,7 +314,12 @@ __device__ __forceinline__ void r16_stage(float2 (&v)[16], Xch &x, const int t, 
   constexpr int Ns = S::F * pow16(ST);
   constexpr int ROW0 = S::F * (pow16(ST) - 1) / 15;
   const int m = t & (Ns - 1);
-#if HOLO_TW_FULL
+#if HOLO_DIT
+  {
+    const float4 a = __ldg(tw + 2 * (ROW0 + m)), b = __ldg(tw + 2 * (ROW0 + m) + 1);
+    dft16_dit_tw<INV>(v, make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y), make_float2(b.z, b.w));
+  }
+#elif HOLO_TW_FULL
   {
     // full table: rows of 8 float4 = 16 float2 (entry 0 unused) per (stage, m)
     const float4 *row = tw + 8 * (ROW0 + m);
@@ -200,13 +353,15 @@ __device__ __forceinline__ void r16_stage(float2 (&v)[16], Xch &x, const int t, 
     twmul<INV>(v[15], cmul(w7, w8));
   }
 #endif
+#if !HOLO_DIT
   dft_reg<16, INV>(v);
+#endif
   if constexpr (ST + 1 < S::S16) {
-    float2 *buf = x.next();
+    float2 *buf = x.next<S::T>();
     const int base = (t - m) * 16 + m;
 #pragma unroll
     for (int s = 0; s < 16; s++) buf[P(base + s * Ns)] = v[s];
-    __syncthreads();
+    x.sync<S::T>();
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = buf[P(t + r * S::T)];
     r16_stage<L, INV, ST + 1>(v, x, t, tw);
@@ -223,16 +378,19 @@ __device__ __forceinline__ void fft(float2 (&v)[16], Xch &x, const int t, const 
     float2 u[F];
 #pragma unroll
     for (int s = 0; s < F; s++) u[s] = v[b + PER * s];
-    dft_reg<F, INV>(u);
+    if constexpr (F == 16 && HOLO_DIT)
+      dft16_dit<INV>(u);
+    else
+      dft_reg<F, INV>(u);
 #pragma unroll
     for (int s = 0; s < F; s++) v[b + PER * s] = u[s];
   }
-  float2 *buf = x.next();
+  float2 *buf = x.next<S::T>();
 #pragma unroll
   for (int b = 0; b < PER; b++)
 #pragma unroll
     for (int s = 0; s < F; s++) buf[P((t + S::T * b) * F + s)] = v[b + PER * s];
-  __syncthreads();
+  x.sync<S::T>();
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = buf[P(t + r * S::T)];
   r16_stage<L, INV, 0>(v, x, t, tw);

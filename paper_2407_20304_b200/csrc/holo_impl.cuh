@@ -46,6 +46,8 @@ struct holo_plan {
   float2 *Qhat = nullptr, *Ghat = nullptr, *Wr = nullptr, *Vr = nullptr, *Href = nullptr, *tw3 = nullptr;
   double *partR = nullptr;
   int ref_cap = 0;  // frames Href / partR are sized for
+  // multiresolution schedule (holo_multires.cuh): up-sampling table [L] and row-pass scratch P2 [L/2][L]
+  float2 *uptab = nullptr, *Up = nullptr;
   // per-pass event profiling (holo_profile_*)
   struct Rec {
     int id;
@@ -82,6 +84,7 @@ struct HoloOps {
                 float2 *wout, const float2 *eta, float2 *gpsi, float2 *gq_out, float gscale, bool want_q, bool acc_q);
   void (*ref_run)(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc);
   void (*ref_fwd)(holo_plan *p, const float2 *q, float2 *w);
+  void (*upsample2)(holo_plan *p, const float2 *coarse, float2 *fine, int count);  // NULL: unsupported L
   int ref_lines_per_cta;  // rows per CTA of the reference-arm row kernels (partials per frame)
 };
 

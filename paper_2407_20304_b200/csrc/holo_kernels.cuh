@@ -56,9 +56,14 @@ struct Cta {
   static constexpr int GS = (HOLO_SINGLE_BUF ? 1 : 2) * LPB + SKEW;
   static constexpr size_t XBYTES = sizeof(float2) * (size_t)GS * G;
   static constexpr size_t PRIV = sizeof(float2) * 16 * NT;  // one thread-private line
+#if HOLO_TMAJOR
+  __device__ __forceinline__ static int g() { return threadIdx.x / T; }
+  __device__ __forceinline__ static int t() { return threadIdx.x % T; }
+#else
   __device__ __forceinline__ static int g() { return threadIdx.x % G; }
   __device__ __forceinline__ static int t() { return threadIdx.x / G; }
-  __device__ __forceinline__ static Xch xch(float2 *sm) { return Xch{sm + (size_t)g() * GS, 0, LPB}; }
+#endif
+  __device__ __forceinline__ static Xch xch(float2 *sm) { return Xch{sm + (size_t)g() * GS, 0, LPB, g()}; }
 };
 
 // P2 layout ("column-pair interleaved") of an R x L complex64 workspace array:
@@ -164,7 +169,10 @@ struct TabPipe {
   __device__ __forceinline__ const float2 *take(const TabSeq &q, bool sync = false) {
     const int i = used++;
     if (i >= 1) {
-      if (sync) __syncthreads();
+      // the slot being refilled held table i - 1: every LINE must be done with it.  The
+      // transforms' barriers guarantee that only within a line when lines sync
+      // independently (HOLO_TMAJOR), so then the CTA syncs here.
+      if (sync || HOLO_TMAJOR) __syncthreads();
       issue(q, i + 1);
     }
     mbar_wait(bar + (i & 1), (i >> 1) & 1);

@@ -12,6 +12,7 @@
 
 #include "holo_impl.cuh"
 #include "holo_passes.cuh"  // only the non-template helpers (k_reduce, k_dots, k_cg) are instantiated here
+#include "holo_multires.cuh"  // k_bin2
 
 using namespace holo;
 using cd = std::complex<double>;
@@ -243,6 +244,10 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   A(&p->partF, sizeof(double) * Kc * nz * p->nbx2);
   A(&p->partX3, sizeof(double) * Kc * 2 * p->nbx3);
   A(&p->partQ, sizeof(double) * 2 * 1184);
+  if (chain_L(L)) {  // multiresolution: up-sampling table and the row-pass scratch P2 [L/2][L]
+    A(&p->uptab, sizeof(float2) * L);
+    A(&p->Up, sizeof(float2) * LL / 2);
+  }
   if (s != HOLO_OK) { holo_plan_destroy(p); return s; }
   // ---- tables (fp64 -> fp32)
   {
@@ -297,6 +302,13 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
       }
     }
     if (chain_L(L)) {
+      // up[F] = [Fbar in [-L/4, L/4)] e^{-i pi Fbar / L} / (L/2): Fourier 2x upsampling from L/2 (O15)
+      std::vector<cd> up(L);
+      for (int f = 0; f < L; f++) {
+        const long fb = fbar(f, L);
+        up[f] = (fb >= -(L / 4) && fb < L / 4) ? expi2pi_frac(-(double)fb / (2.0 * L)) / (double)(L / 2) : cd(0, 0);
+      }
+      if (s == HOLO_OK) s = upload(p, p->uptab, up);
       if (s == HOLO_OK) s = upload(p, p->hdet, hd);
       if (s == HOLO_OK) s = upload(p, p->homega, ho);
       if (s == HOLO_OK) s = upload(p, p->cout, co);
@@ -491,6 +503,27 @@ holo_status holo_fwd_ref(holo_plan *p, const void *q, void *w) {
   if (!q || (p->n_ref > 0 && !w)) return fail(p, HOLO_EINVAL, "null pointer");
   if (p->n_ref == 0) return HOLO_OK;
   p->ops->ref_fwd(p, (const float2 *)q, (float2 *)w);
+  return postcheck(p);
+}
+
+holo_status holo_upsample2(holo_plan *p, const void *coarse, void *fine, int32_t count) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (count < 0 || (count > 0 && (!coarse || !fine))) return fail(p, HOLO_EINVAL, "bad upsample2 arguments");
+  if (!p->ops->upsample2) return fail(p, HOLO_EUNSUPPORTED, "upsample2 needs a power-of-two npad");
+  if (count == 0) return HOLO_OK;
+  p->ops->upsample2(p, (const float2 *)coarse, (float2 *)fine, count);
+  return postcheck(p);
+}
+
+holo_status holo_bin2(holo_plan *p, const float *fine, float *coarse, int32_t count) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (count < 0 || (count > 0 && (!fine || !coarse))) return fail(p, HOLO_EINVAL, "bad bin2 arguments");
+  if (count == 0) return HOLO_OK;
+  pbeg(p);
+  k_bin2<<<1184, 256, 0, p->stream>>>(fine, coarse, p->N, (size_t)count);
+  pend(p, HOLO_PASS_FILTER, 20.0 * count * (double)p->N * p->N, 0);
   return postcheck(p);
 }
 

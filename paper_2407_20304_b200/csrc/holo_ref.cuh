@@ -58,7 +58,7 @@ struct LineEng<6144> {
   };
   __device__ __forceinline__ static St init(float2 *sm) {
     const int g3 = threadIdx.x / 128, t = threadIdx.x % 128;
-    return St{Xch{sm + (size_t)g3 * GS, 0, CS::LPB}, t, 0, g3, sm};
+    return St{Xch{sm + (size_t)g3 * GS, 0, CS::LPB, g3}, t, 0, g3, sm};  // sub-line g3 = warps 4 g3 .. 4 g3 + 3
   }
   __device__ __forceinline__ static int isp(const St &s, int r) { return 3 * (s.t + r * T) + s.g3; }
   __device__ __forceinline__ static int ifr(const St &s, int r) { return s.t + r * T + LS * s.g3; }

@@ -8,6 +8,7 @@
 #pragma once
 #include "holo_impl.cuh"
 #include "holo_passes.cuh"
+#include "holo_multires.cuh"
 #include "holo_ref.cuh"
 
 namespace holo_run {
@@ -36,6 +37,8 @@ void set_chain_attrs() {
   a((const void *)k_rows_filter<L, true, false, false>, S::X);
   a((const void *)k_rows_filter<L, true, false, true>, S::X);
   a((const void *)k_cols_filter<L>, S::X);
+  a((const void *)k_up_rows<L>, S::X);
+  a((const void *)k_up_cols<L>, S::X);
 }
 
 template <int L>
@@ -94,6 +97,18 @@ struct Run {
       else
         k_rows_filter<L, true, false, false><<<L / G, NT, SM::X, p->stream>>>(Gj, out, tb, p->homega + j * L, 1, scale);
       pend(p, HOLO_PASS_FILTER, (acc ? 5 : 4) * A, 4.0 * L * fftf(L), 2);
+    }
+  }
+
+  // Fourier 2x upsampling of count coarse [L/2][L/2] fields to [L][L] (O15, holo_multires.cuh)
+  static void upsample2(holo_plan *p, const float2 *coarse, float2 *fine, int count) {
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const size_t Lc2 = (size_t)(L / 2) * (L / 2);
+    for (int m = 0; m < count; m++) {
+      pbeg(p);
+      k_up_rows<L><<<(L / 2) / G, NT, SM::X, p->stream>>>(coarse + m * Lc2, p->Up, tw, p->uptab);
+      k_up_cols<L><<<L / G, NT, SM::X, p->stream>>>(p->Up, fine + m * (size_t)L * L, tw, p->uptab);
+      pend(p, HOLO_PASS_FILTER, A / 4 + A / 2 + A / 2 + A, 2.0 * (L / 2 + L) * fftf(L), 2);
     }
   }
 
@@ -304,9 +319,14 @@ struct RefRun {
     holo_run::set_ref_attrs<LV>();                                                                              \
     holo_run::set_chain_attrs<LV>();                                                                            \
   }                                                                                                             \
-  extern const HoloOps holo_ops_##LV = {LV, holo_set_attrs_##LV, holo_run::Run<LV>::sweep,                      \
-                                        holo_run::RefRun<LV>::run, holo_run::RefRun<LV>::fwd, holo::LineEng<LV>::G};
+  extern const HoloOps holo_ops_##LV = {LV,                                                                    \
+                                        holo_set_attrs_##LV,                                                   \
+                                        holo_run::Run<LV>::sweep,                                              \
+                                        holo_run::RefRun<LV>::run,                                             \
+                                        holo_run::RefRun<LV>::fwd,                                             \
+                                        holo_run::Run<LV>::upsample2,                                          \
+                                        holo::LineEng<LV>::G};
 #define HOLO_DEFINE_REF_OPS(LV)                                                                                  \
   static void holo_set_attrs_##LV() { holo_run::set_ref_attrs<LV>(); }                                          \
-  extern const HoloOps holo_ops_##LV = {LV, holo_set_attrs_##LV, nullptr, holo_run::RefRun<LV>::run,            \
-                                        holo_run::RefRun<LV>::fwd, holo::LineEng<LV>::G};
+  extern const HoloOps holo_ops_##LV = {LV,      holo_set_attrs_##LV,       nullptr, holo_run::RefRun<LV>::run, \
+                                        holo_run::RefRun<LV>::fwd, nullptr, holo::LineEng<LV>::G};
