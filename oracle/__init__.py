@@ -65,6 +65,8 @@ def _load():
         lib.or_grad_ref.restype = D
         lib.or_upsample2.argtypes = [Ic, P, P]
         lib.or_bin2.argtypes = [Ic, Ic, P, P]
+        lib.or_init_probe.argtypes = [Ic, Ic, Ic, D, D, D, P, P, P]
+        lib.or_multipaganin.argtypes = [Ic, Ic, Ic, D, D, P, P, P, P, P, D, P]
         _lib = lib
     return _lib
 
@@ -225,4 +227,27 @@ def bin2(a):
     M, N = a.shape[0], a.shape[-1] // 2
     out = np.empty((M, N, N), np.float64)
     _load().or_bin2(M, N, _p(a), _p(out))
+    return out
+
+
+def init_probe(geom: Geometry, ref_shifts, sqrt_dref, L):
+    """O17: q0 = (1/R) sum_r S_{-s_r} P_{-zeta0} Z_{c_r}(sqrt d~^r_r), ring = frame mean (reading R3)."""
+    sqrt_dref = _c(sqrt_dref, np.float64)
+    R, N = sqrt_dref.shape[0], sqrt_dref.shape[-1]
+    rs = _c(ref_shifts, np.float64).reshape(R, 2)
+    q0 = np.empty((L, L), np.complex128)
+    _load().or_init_probe(R, L, N, geom.wavelength, geom.p0, float(geom.zeta[0]), _p(rs), _p(sqrt_dref), _p(q0))
+    return q0
+
+
+def multipaganin(geom: Geometry, L, shifts_k, sqrt_d_k, sqrt_dref, delta_beta):
+    """O18: multi-distance Paganin initial object of one angle (reading R4); shifts_k [nz][2],
+    sqrt_d_k [nz][N][N], sqrt_dref [N][N]."""
+    sqrt_d_k = _c(sqrt_d_k, np.float64)
+    sqrt_dref = _c(sqrt_dref, np.float64)
+    sk = _c(shifts_k, np.float64).reshape(geom.nz, 2)
+    N = sqrt_dref.shape[-1]
+    out = np.empty((L, L), np.complex128)
+    _load().or_multipaganin(geom.nz, L, N, geom.wavelength, geom.p0, _p(geom.mt), _p(geom.zeta), _p(sk),
+                            _p(sqrt_d_k), _p(sqrt_dref), float(delta_beta), _p(out))
     return out

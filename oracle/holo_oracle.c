@@ -457,3 +457,89 @@ void or_bin2(int count, int N, const double *fine, double *coarse) {
         coarse[c * (long)N * N + i * N + l] = sqrt(0.25 * s);
       }
 }
+
+/* plain DFT line ops for apply_axis (ctx = the twiddle table W) */
+static void dft_fwd_line(const void *c, long L, const cplx *in, cplx *out, cplx *sc) {
+  (void)sc;
+  dft_line(L, 0, (const cplx *)c, in, out);
+}
+static void dft_inv_line(const void *c, long L, const cplx *in, cplx *out, cplx *sc) {
+  (void)sc;
+  dft_line(L, 1, (const cplx *)c, in, out);
+}
+
+/* ------------------------------------------------------------------ O17 --- */
+/* Initial probe ("the reference image propagated back to the sample
+ * plane 0"; reference model P:102, Eq. (10)):
+ *   q0 = (1/R) sum_r S_{-s_r} P_{-zeta0} Z_{c_r}(a_r),  a_r = sqrt(d~^r_r),  c_r = mean(a_r)
+ * (zero phase; the ring around the N x N frame filled with the frame's mean amplitude, R3). */
+void or_init_probe(int R, int L, int N, double lam, double p0, double zeta0, const double *ref_shifts,
+                   const double *sqrt_dref, cplx *q0) {
+  const long LL = (long)L * L, NN = (long)N * N, o = (L - N) / 2;
+  cplx *t = (cplx *)malloc(sizeof(cplx) * LL);
+  for (long i = 0; i < LL; i++) q0[i] = 0;
+  for (int r = 0; r < R; r++) {
+    const double *a = sqrt_dref + r * NN;
+    double c = 0;
+    for (long i = 0; i < NN; i++) c += a[i];
+    c /= (double)NN;
+    for (long y = 0; y < L; y++)
+      for (long x = 0; x < L; x++) {
+        const int in = y >= o && y < o + N && x >= o && x < o + N;
+        t[y * L + x] = in ? a[(y - o) * N + (x - o)] : c;
+      }
+    or_prop(L, lam, p0, -zeta0, t, t);
+    or_shift(L, -ref_shifts[2 * r], -ref_shifts[2 * r + 1], t, t);
+    for (long i = 0; i < LL; i++) q0[i] += t[i] / (double)R;
+  }
+  free(t);
+}
+
+/* ------------------------------------------------------------------ O18 --- */
+/* Multi-distance Paganin (TIE) initial object of one angle (formula absent from
+ * the paper: SPEC's documented stand-in in this build's sign convention, reading R4):
+ *   R_j = (a_kj / a^r)^2, a^r^2 floored at 1e-6 max, padded with 1;
+ *   I_j = M_{1/mt'} S_{s'} R_j,  mt' = 1/mt_j, s' = -s_kj / mt_j            (O5)
+ *   Phi = sum_j DFT2(I_j) / (nz + pi lambda db sum_j zeta_j |f|^2),  |f| = fbar/(L p0)
+ *   phi = (db/2) ln max(Re IDFT2(Phi), 1e-6),  psi0 = exp((i + 1/db) phi).               */
+void or_multipaganin(int nz, int L, int N, double lam, double p0, const double *mt, const double *zeta,
+                     const double *shifts_k, const double *sqrt_d_k, const double *sqrt_dref, double db,
+                     cplx *psi0) {
+  const long LL = (long)L * L, NN = (long)N * N, o = (L - N) / 2;
+  cplx *t = (cplx *)malloc(sizeof(cplx) * LL), *num = (cplx *)malloc(sizeof(cplx) * LL);
+  cplx *W = twiddles(L);
+  double amax = 0, zs = 0;
+  for (long i = 0; i < NN; i++) amax = fmax(amax, sqrt_dref[i] * sqrt_dref[i]);
+  for (int j = 0; j < nz; j++) zs += zeta[j];
+  for (long i = 0; i < LL; i++) num[i] = 0;
+  for (int j = 0; j < nz; j++) {
+    for (long y = 0; y < L; y++)
+      for (long x = 0; x < L; x++) {
+        const int in = y >= o && y < o + N && x >= o && x < o + N;
+        double v = 1.0;
+        if (in) {
+          const long i = (y - o) * N + (x - o);
+          const double ar2 = fmax(sqrt_dref[i] * sqrt_dref[i], 1e-6 * amax);
+          v = sqrt_d_k[j * NN + i] * sqrt_d_k[j * NN + i] / ar2;
+        }
+        t[y * L + x] = v;
+      }
+    const double mtp = 1.0 / mt[j];
+    or_mag(L, mtp, -shifts_k[2 * j] * mtp, -shifts_k[2 * j + 1] * mtp, t, t);
+    apply_axis(L, 0, t, t, dft_fwd_line, W);
+    apply_axis(L, 1, t, t, dft_fwd_line, W);
+    for (long i = 0; i < LL; i++) num[i] += t[i];
+  }
+  for (long fy = 0; fy < L; fy++)
+    for (long fx = 0; fx < L; fx++) {
+      const double gy = (double)fbar_of(fy, L) / ((double)L * p0), gx = (double)fbar_of(fx, L) / ((double)L * p0);
+      num[fy * L + fx] /= (double)nz + PI * lam * db * zs * (gx * gx + gy * gy);
+    }
+  apply_axis(L, 0, num, num, dft_inv_line, W);
+  apply_axis(L, 1, num, num, dft_inv_line, W);
+  for (long i = 0; i < LL; i++) {
+    const double phi = 0.5 * db * log(fmax(creal(num[i]), 1e-6));
+    psi0[i] = cexp((I + 1.0 / db) * phi);
+  }
+  free(t); free(num); free(W);
+}

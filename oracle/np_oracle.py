@@ -209,3 +209,51 @@ def bin2(a):
     a = np.asarray(a, np.float64)
     s = a[..., 0::2, 0::2] ** 2 + a[..., 1::2, 0::2] ** 2 + a[..., 0::2, 1::2] ** 2 + a[..., 1::2, 1::2] ** 2
     return np.sqrt(0.25 * s)
+
+
+def pad_const(a, L, c):
+    """Z_c: the N x N frame a centred on the L x L torus, the ring filled with the constant c."""
+    N = a.shape[-1]
+    o = (L - N) // 2
+    out = np.full(a.shape[:-2] + (L, L), c, np.complex128)
+    out[..., o:o + N, o:o + N] = a
+    return out
+
+
+def init_probe(wavelength, p0, zeta0, ref_shifts, sqrt_dref, L):
+    """O17 (P:147, P:241, P:272 "the reference image propagated back to the sample plane 0";
+    reference model |P_{zeta0} S_{s_r} q|^2 = d~^r, P:102 / Eq. (10)):
+        q0 = (1/R) sum_r S_{-s_r} P_{-zeta0} Z_{c_r}(sqrt d~^r_r),  c_r = mean of sqrt d~^r_r,
+    the amplitude with zero phase, each frame padded with its mean amplitude (reading R3)."""
+    R = sqrt_dref.shape[0]
+    q0 = np.zeros((L, L), np.complex128)
+    for r in range(R):
+        a = np.asarray(sqrt_dref[r], np.float64)
+        x = pad_const(a, L, a.mean())
+        q0 += shift(prop(x, wavelength, p0, -zeta0), -float(ref_shifts[r][0]), -float(ref_shifts[r][1]))
+    return q0 / R
+
+
+def multipaganin(geom, L, shifts_k, sqrt_d_k, sqrt_dref, delta_beta):
+    """O18: multi-distance Paganin (TIE) initial object for one angle (the formula is
+    absent from the paper -- SPEC's documented stand-in, in this build's sign convention, reading R4):
+      R_j = (sqrt_d_kj / sqrt_dref)^2 (flat-field; sqrt_dref^2 floored at 1e-6 max), padded with 1;
+      I_j = M_{1/mt'} S_{s'} R_j with mt' = 1/mt_j, s' = -s_kj/mt_j   (O5: undo the plane's
+            magnification and shift, so I_j ~ |P_{zeta_j} psi_k|^2 on the psi grid, Eq. (7) P:87-90);
+      Phi = sum_j DFT2(I_j) / (N_z + pi lambda delta_beta sum_j zeta_j |f|^2),  |f| = fbar / (L p0);
+      phi = (delta_beta / 2) ln max(Re IDFT2(Phi), 1e-6);   psi0 = exp((i + 1/delta_beta) phi)."""
+    nz = geom.nz
+    a_r2 = np.asarray(sqrt_dref, np.float64) ** 2
+    a_r2 = np.maximum(a_r2, 1e-6 * a_r2.max())
+    fb = fbar(L) / (L * geom.p0)
+    f2 = fb[:, None] ** 2 + fb[None, :] ** 2
+    num = np.zeros((L, L), np.complex128)
+    for j in range(nz):
+        Rj = pad_const(np.asarray(sqrt_d_k[j], np.float64) ** 2 / a_r2, L, 1.0)
+        mtp = 1.0 / geom.mt[j]
+        Ij = MagOp(L, mtp).fwd(Rj, -shifts_k[j][0] * mtp, -shifts_k[j][1] * mtp)
+        num += np.fft.fft2(Ij)
+    den = nz + np.pi * geom.wavelength * delta_beta * float(np.sum(geom.zeta)) * f2
+    T = np.real(np.fft.ifft2(num / den))
+    phi = 0.5 * delta_beta * np.log(np.maximum(T, 1e-6))
+    return np.exp((1j + 1.0 / delta_beta) * phi)
