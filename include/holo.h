@@ -174,6 +174,21 @@ holo_status holo_cg_step(holo_plan *p, const holo_cg_in *in /*[host]*/, holo_cg_
 holo_status holo_upsample2(holo_plan *p, const void *coarse, void *fine, int32_t count);
 holo_status holo_bin2(holo_plan *p, const float *fine, float *coarse, int32_t count);
 
+/* Initialisers.
+ * holo_init_probe (O17): "the reference image propagated back to the sample plane 0":
+ *   q0 = (1/R) sum_r S_{-s_r} P_{-zeta0} Z_{c_r}(sqrt_dref_r)   [npad][npad] complex64,
+ *   sqrt_dref [R][n][n] (R = n_ref, shifts of holo_set_ref_shifts), each frame padded with its
+ *   mean amplitude c_r (reading R3).  HOLO_EINVAL without reference frames.
+ * holo_init_psi (O18): multi-distance Paganin initial object of every angle (reading R4):
+ *   R_j = (sqrt_d_kj / sqrt_dref)^2 (sqrt_dref^2 floored at 1e-6 of its max), 1 outside the data;
+ *   I_j = M_{mt_j} S_{-s_kj} R_j on the psi grid (O5 with mt' = 1/mt_j, s' = -s_kj/mt_j);
+ *   phi = (db/2) ln Re IDFT2[ sum_j DFT2(I_j) / (nz + pi lambda db sum_j zeta_j |f|^2) ];
+ *   psi0_k = exp((i + 1/db) phi).  sqrt_d [K][nz][n][n], sqrt_dref [n][n] (the flat field of
+ *   every plane), delta_beta = delta/beta > 0, psi0 [K][npad][npad].  Uses the plan's
+ *   shifts (holo_set_shifts) and its T1/T3 workspace; power-of-two npad only. */
+holo_status holo_init_probe(holo_plan *p, const float *sqrt_dref, void *q0);
+holo_status holo_init_psi(holo_plan *p, const float *sqrt_d, const float *sqrt_dref, double delta_beta, void *psi0);
+
 /* Number of kernel launches this plan has enqueued since creation (profiling aid). */
 uint64_t holo_launch_count(const holo_plan *p);
 

@@ -87,6 +87,11 @@ _lib.holo_upsample2.restype = _S
 _lib.holo_bin2.argtypes = [_P, _P, _P, ctypes.c_int32]
 _lib.holo_bin2.restype = _S
 
+_lib.holo_init_probe.argtypes = [_P, _P, _P]
+_lib.holo_init_probe.restype = _S
+_lib.holo_init_psi.argtypes = [_P, _P, _P, ctypes.c_double, _P]
+_lib.holo_init_psi.restype = _S
+
 _lib.holo_profile_enable.argtypes = [_P, ctypes.c_int]
 _lib.holo_profile_enable.restype = _S
 _lib.holo_profile_read.argtypes = [_P, _P, _P, _P, _P, ctypes.c_int]
@@ -100,7 +105,7 @@ PASS_KERNELS = ["k_x1", "k_y1", "k_x2", "k_y2", "k_x3", "k_rows_filter|k_cols_fi
 EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes", "holo_last_error",
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
             "holo_grad_ref", "holo_fwd_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
-            "holo_profile_read", "holo_upsample2", "holo_bin2"]
+            "holo_profile_read", "holo_upsample2", "holo_bin2", "holo_init_probe", "holo_init_psi"]
 
 
 class HoloError(RuntimeError):
@@ -273,3 +278,18 @@ class Plan:
         self._chk(_lib.holo_bin2(self._h, _ptr(fine, torch.float32, M * 4 * self.n ** 2, "fine"),
                                  _ptr(coarse, torch.float32, M * self.n ** 2, "coarse"), M))
         return coarse
+
+    # ---- initialisers
+    def init_probe(self, sqrt_dref, q0):
+        """holo_init_probe (O17): q0 from the n_ref reference frames sqrt_dref [R][n][n]."""
+        self._chk(_lib.holo_init_probe(self._h, _ptr(sqrt_dref, torch.float32, self.n_ref * self.n ** 2, "sqrt_dref"),
+                                       _ptr(q0, torch.complex64, self.npad ** 2, "q0")))
+        return q0
+
+    def init_psi(self, sqrt_d, sqrt_dref, delta_beta, psi0):
+        """holo_init_psi (O18): multi-distance Paganin psi0 [K][npad][npad] from sqrt_d [K][nz][n][n] and the
+        flat field sqrt_dref [n][n]."""
+        self._chk(_lib.holo_init_psi(self._h, _ptr(sqrt_d, torch.float32, self.K * self.nz * self.n ** 2, "sqrt_d"),
+                                     _ptr(sqrt_dref, torch.float32, self.n ** 2, "sqrt_dref"), float(delta_beta),
+                                     _ptr(psi0, torch.complex64, self.K * self.npad ** 2, "psi0")))
+        return psi0

@@ -48,6 +48,9 @@ struct holo_plan {
   int ref_cap = 0;  // frames Href / partR are sized for
   // multiresolution schedule (holo_multires.cuh): up-sampling table [L] and row-pass scratch P2 [L/2][L]
   float2 *uptab = nullptr, *Up = nullptr;
+  // initial object (O18, holo_init.cuh): inverse-magnification Bluestein tables [nz][L] (mt' = 1/mt_j)
+  float2 *pcin = nullptr, *pcout = nullptr, *pbke = nullptr, *pbko = nullptr;
+  std::vector<double> shifts_host;  // [K][nz][2] as last set by holo_set_shifts
   // per-pass event profiling (holo_profile_*)
   struct Rec {
     int id;
@@ -85,6 +88,8 @@ struct HoloOps {
   void (*ref_run)(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc);
   void (*ref_fwd)(holo_plan *p, const float2 *q, float2 *w);
   void (*upsample2)(holo_plan *p, const float2 *coarse, float2 *fine, int count);  // NULL: unsupported L
+  void (*init_psi)(holo_plan *p, const float *sqrt_d, const float *sqrt_dref, double db, float2 *psi0);  // O18
+  void (*init_probe)(holo_plan *p, const float *sqrt_dref, float2 *q0);                               // O17
   int ref_lines_per_cta;  // rows per CTA of the reference-arm row kernels (partials per frame)
 };
 

@@ -134,6 +134,37 @@ std::vector<cd> transfer(int L, double lam, double p0, double z) {
   return h;
 }
 
+// Bluestein chirp-z tables of M_{1/mt} on an L torus (reading C1, holo_kernels.cuh mag_fwd), appended:
+//   cin[f]  = kappa (-1)^fbar e^{i pi mt fbar^2 / L} / L      (kappa: -L/2 <= mt fbar < L/2)
+//   cout[o] = e^{i pi mt (o - L/2)^2 / L}
+//   b[d] = e^{-i pi mt d^2 / L}, |d| < L, on a 2L cycle; Bhat = FFT_2L(b) / (2L) split even / odd
+// phases reduced in cycles in fp64 before rounding.
+void czt_tables(int L, double mt, std::vector<cd> &cin, std::vector<cd> &co, std::vector<cd> &be,
+                std::vector<cd> &bo) {
+  for (int f = 0; f < L; f++) {
+    long fb = fbar(f, L);
+    double v = mt * (double)fb;
+    bool kap = v >= -(double)(L / 2) && v < (double)(L / 2);
+    double cyc = std::fmod(mt * (double)(fb * fb), 2.0 * L) / (2.0 * L) + (fb & 1 ? 0.5 : 0.0);
+    cin.push_back(kap ? expi2pi_frac(cyc) / (double)L : cd(0, 0));
+  }
+  for (int o = 0; o < L; o++) {
+    long n = o - L / 2;
+    co.push_back(expi2pi_frac(std::fmod(mt * (double)(n * n), 2.0 * L) / (2.0 * L)));
+  }
+  std::vector<cd> b(2 * L, cd(0, 0));
+  for (int d = 0; d < L; d++) {
+    cd v = expi2pi_frac(-std::fmod(mt * (double)((long)d * d), 2.0 * L) / (2.0 * L));
+    b[d] = v;
+    if (d > 0) b[2 * L - d] = v;
+  }
+  fft64(b);
+  for (int kk = 0; kk < L; kk++) {
+    be.push_back(b[2 * kk] / (2.0 * L));
+    bo.push_back(b[2 * kk + 1] / (2.0 * L));
+  }
+}
+
 bool supported_L(int L) {
   return L == 128 || L == 256 || L == 512 || L == 1024 || L == 2048 || L == 4096 || L == 6144;
 }
@@ -244,6 +275,12 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   A(&p->partF, sizeof(double) * Kc * nz * p->nbx2);
   A(&p->partX3, sizeof(double) * Kc * 2 * p->nbx3);
   A(&p->partQ, sizeof(double) * 2 * 1184);
+  if (chain_L(L) && K > 0) {  // initial object (O18): inverse-magnification chirp-z tables
+    A(&p->pcin, sizeof(float2) * L * nz);
+    A(&p->pcout, sizeof(float2) * L * nz);
+    A(&p->pbke, sizeof(float2) * L * nz);
+    A(&p->pbko, sizeof(float2) * L * nz);
+  }
   if (chain_L(L)) {  // multiresolution: up-sampling table and the row-pass scratch P2 [L/2][L]
     A(&p->uptab, sizeof(float2) * L);
     A(&p->Up, sizeof(float2) * LL / 2);
@@ -259,7 +296,7 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
         for (int e : {1, 2, 4, 8}) tw.push_back(expi2pi_frac(-(double)((long)m * e) / (16.0 * Ns)));
     if (tw.size() != 4 * twrows) { holo_plan_destroy(p); return HOLO_EUNSUPPORTED; }
     if (s == HOLO_OK) s = upload(p, p->tw, tw);
-    std::vector<cd> hd, ho, co, be, bo;
+    std::vector<cd> hd, ho, co, be, bo, pci, pco, pbe, pbo;
     p->cin_host.clear();
     if (!chain_L(L)) {  // radix-3 combine twiddles W_6144^{g k}, g = 1, 2 (holo_ref.cuh)
       std::vector<cd> t3;
@@ -274,32 +311,8 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
       auto h2 = transfer(L, g->wavelength, p->p0, p->omega[j]);
       hd.insert(hd.end(), h1.begin(), h1.end());
       ho.insert(ho.end(), h2.begin(), h2.end());
-      const double mt = p->mt[j];
-      // cin[f] = kappa (-1)^fbar e^{i pi mt fbar^2 / L} / L ; phase in cycles: mt fbar^2 / (2L)
-      for (int f = 0; f < L; f++) {
-        long fb = fbar(f, L);
-        double v = mt * (double)fb;
-        bool kap = v >= -(double)(L / 2) && v < (double)(L / 2);
-        double cyc = std::fmod(mt * (double)(fb * fb), 2.0 * L) / (2.0 * L) + (fb & 1 ? 0.5 : 0.0);
-        p->cin_host.push_back(kap ? expi2pi_frac(cyc) / (double)L : cd(0, 0));
-      }
-      for (int o = 0; o < L; o++) {
-        long n = o - L / 2;
-        cd c = expi2pi_frac(std::fmod(mt * (double)(n * n), 2.0 * L) / (2.0 * L));
-        co.push_back(c);
-      }
-      // b[d] = exp(-i pi mt d^2 / L), |d| < L, on a 2L cycle; Bhat = FFT_2L(b) / (2L)
-      std::vector<cd> b(2 * L, cd(0, 0));
-      for (int d = 0; d < L; d++) {
-        cd v = expi2pi_frac(-std::fmod(mt * (double)((long)d * d), 2.0 * L) / (2.0 * L));
-        b[d] = v;
-        if (d > 0) b[2 * L - d] = v;
-      }
-      fft64(b);
-      for (int kk = 0; kk < L; kk++) {
-        be.push_back(b[2 * kk] / (2.0 * L));
-        bo.push_back(b[2 * kk + 1] / (2.0 * L));
-      }
+      czt_tables(L, p->mt[j], p->cin_host, co, be, bo);
+      if (K > 0) czt_tables(L, 1.0 / p->mt[j], pci, pco, pbe, pbo);  // O18: inverse magnification
     }
     if (chain_L(L)) {
       // up[F] = [Fbar in [-L/4, L/4)] e^{-i pi Fbar / L} / (L/2): Fourier 2x upsampling from L/2 (O15)
@@ -314,11 +327,17 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
       if (s == HOLO_OK) s = upload(p, p->cout, co);
       if (s == HOLO_OK) s = upload(p, p->bke, be);
       if (s == HOLO_OK) s = upload(p, p->bko, bo);
+      if (K > 0) {
+        if (s == HOLO_OK) s = upload(p, p->pcin, pci);
+        if (s == HOLO_OK) s = upload(p, p->pcout, pco);
+        if (s == HOLO_OK) s = upload(p, p->pbke, pbe);
+        if (s == HOLO_OK) s = upload(p, p->pbko, pbo);
+      }
     }
   }
   if (s == HOLO_OK && K > 0) {  // zero shifts until holo_set_shifts
-    std::vector<double> zero((size_t)K * nz * 2, 0.0);
-    s = upload_cr(p, zero.data());
+    p->shifts_host.assign((size_t)K * nz * 2, 0.0);
+    s = upload_cr(p, p->shifts_host.data());
   }
   if (s != HOLO_OK) { holo_plan_destroy(p); return s; }
   *out = p;
@@ -381,6 +400,7 @@ holo_status holo_set_shifts(holo_plan *p, const double *s) {
   const int L = p->L, nz = p->nz, K = p->K;
   for (size_t i = 0; i < (size_t)K * nz * 2; i++)
     if (!std::isfinite(s[i]) || std::fabs(s[i]) >= L / 2) return fail(p, HOLO_EINVAL, "shift not finite or >= npad/2");
+  p->shifts_host.assign(s, s + (size_t)K * nz * 2);
   return upload_cr(p, s);
 }
 
@@ -524,6 +544,26 @@ holo_status holo_bin2(holo_plan *p, const float *fine, float *coarse, int32_t co
   pbeg(p);
   k_bin2<<<1184, 256, 0, p->stream>>>(fine, coarse, p->N, (size_t)count);
   pend(p, HOLO_PASS_FILTER, 20.0 * count * (double)p->N * p->N, 0);
+  return postcheck(p);
+}
+
+holo_status holo_init_probe(holo_plan *p, const float *sqrt_dref, void *q0) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!q0 || (p->n_ref > 0 && !sqrt_dref)) return fail(p, HOLO_EINVAL, "null pointer");
+  if (p->n_ref == 0) return fail(p, HOLO_EINVAL, "no reference frames (holo_set_ref_shifts)");
+  p->ops->init_probe(p, sqrt_dref, (float2 *)q0);
+  return postcheck(p);
+}
+
+holo_status holo_init_psi(holo_plan *p, const float *sqrt_d, const float *sqrt_dref, double delta_beta, void *psi0) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!sqrt_d || !sqrt_dref || !psi0) return fail(p, HOLO_EINVAL, "null pointer");
+  if (!(delta_beta > 0) || !std::isfinite(delta_beta)) return fail(p, HOLO_EINVAL, "delta_beta must be > 0");
+  if (p->K == 0) return HOLO_OK;
+  if (!p->ops->init_psi) return fail(p, HOLO_EUNSUPPORTED, "init_psi needs a power-of-two npad");
+  p->ops->init_psi(p, sqrt_d, sqrt_dref, delta_beta, (float2 *)psi0);
   return postcheck(p);
 }
 

@@ -107,7 +107,7 @@ struct LineEng<6144> {
   }
 };
 
-enum { REF_QHAT = 0, REF_R1 = 1, REF_R2 = 2, REF_R3 = 3, REF_FINAL = 4, REF_FWD = 5 };
+enum { REF_QHAT = 0, REF_R1 = 1, REF_R2 = 2, REF_R3 = 3, REF_FINAL = 4, REF_FWD = 5, REF_INIT = 6 };
 
 // ---------------------------------------------------------------- column passes
 // QHAT : Qx (P2, spectral x / spatial y) -> forward along y -> Qhat (P2), in place
@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
 //        forward along x -> x conj(Hx) -> V (P2, N rows); partial[blk] = F of the CTA
 // FINAL: Ghat row (P2) -> inverse along x -> out (row-major) (+)= scale v
 // FWD  : W row (P2, N rows) x Hx -> inverse along x -> crop -> w frame (row-major N x N)
+// INIT : (a - mean) row (partial = &mean, fp64), zero-padded -> forward along x -> x conj(Hx) -> V
 template <int L, int MODE>
 __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     k_ref_rows(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
@@ -221,6 +222,24 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     }
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0) partial[blockIdx.x] = s;
+    E::fwd(v, st, tw, tw3);
+    if (act) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) {
+        const int f = E::ifr(st, r);
+        out[p2(y, f, N)] = cmulc(v[r], ldg2(Hx + f));
+      }
+    }
+  } else if (MODE == REF_INIT) {
+    // O17 (initial probe): the frame's amplitude minus its mean c (partial[0], fp64), zero-padded,
+    // forward along x, x conj(Hx) -> V (P2, N rows); R3 + FINAL then give S_{-s} P_{-zeta0} Z (a - c)
+    const bool act = y < N;
+    const float c = (float)partial[0];
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int cc = E::isp(st, r) - o;
+      v[r] = make_float2((act && cc >= 0 && cc < N) ? __ldg(sqrt_d + (size_t)y * N + cc) - c : 0.f, 0.f);
+    }
     E::fwd(v, st, tw, tw3);
     if (act) {
 #pragma unroll

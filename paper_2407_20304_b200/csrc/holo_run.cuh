@@ -9,6 +9,7 @@
 #include "holo_impl.cuh"
 #include "holo_passes.cuh"
 #include "holo_multires.cuh"
+#include "holo_init.cuh"
 #include "holo_ref.cuh"
 
 namespace holo_run {
@@ -39,6 +40,9 @@ void set_chain_attrs() {
   a((const void *)k_cols_filter<L>, S::X);
   a((const void *)k_up_rows<L>, S::X);
   a((const void *)k_up_cols<L>, S::X);
+  a((const void *)k_pag_rows<L>, S::XPT);
+  a((const void *)k_pag_cols<L>, S::XPT);
+  a((const void *)k_pag_final<L>, S::X);
 }
 
 template <int L>
@@ -53,6 +57,7 @@ void set_ref_attrs() {
   a((const void *)k_ref_rows<L, REF_R2>);
   a((const void *)k_ref_rows<L, REF_FINAL>);
   a((const void *)k_ref_rows<L, REF_FWD>);
+  a((const void *)k_ref_rows<L, REF_INIT>);
 }
 
 // ------------------------------------------------------------------ object chain
@@ -109,6 +114,39 @@ struct Run {
       k_up_rows<L><<<(L / 2) / G, NT, SM::X, p->stream>>>(coarse + m * Lc2, p->Up, tw, p->uptab);
       k_up_cols<L><<<L / G, NT, SM::X, p->stream>>>(p->Up, fine + m * (size_t)L * L, tw, p->uptab);
       pend(p, HOLO_PASS_FILTER, A / 4 + A / 2 + A / 2 + A, 2.0 * (L / 2 + L) * fftf(L), 2);
+    }
+  }
+
+  // O18: multi-distance Paganin initial object of every angle (holo_init.cuh)
+  static void init_psi(holo_plan *p, const float *sqrt_d, const float *sqrt_dref, double db, float2 *psi0) {
+    const Tables tb = p->tables();
+    const int N = p->N, nz = p->nz;
+    const size_t NN = (size_t)N * N, LL = (size_t)L * L;
+    double zs = 0;
+    for (int j = 0; j < nz; j++) zs += p->zeta[j];
+    const double kPi = 3.14159265358979323846;
+    const float cden = (float)(kPi * p->g.wavelength * db * zs / ((L * p->p0) * (L * p->p0)));
+    TabSeq seq{};
+    for (int j = 0; j < nz; j++) {
+      const float2 *list[5] = {p->pcin + (size_t)j * L, p->pbke + (size_t)j * L, p->pcin + (size_t)j * L,
+                               p->pbko + (size_t)j * L, p->pcout + (size_t)j * L};
+      for (auto *e : list) seq.p[seq.n++] = e;
+    }
+    pbeg(p);
+    k_frame_stats<<<1, 256, 0, p->stream>>>(sqrt_dref, NN, nullptr, p->partQ);
+    pend(p, HOLO_PASS_REDUCE, 4.0 * NN, 0);
+    for (int k = 0; k < p->K; k++) {
+      PagArgs pa{};
+      for (int j = 0; j < nz; j++) {
+        pa.sx[j] = (float)(-p->shifts_host[((size_t)k * nz + j) * 2] / p->mt[j]);
+        pa.sy[j] = (float)(-p->shifts_host[((size_t)k * nz + j) * 2 + 1] / p->mt[j]);
+      }
+      pbeg(p);
+      k_pag_rows<L><<<L / G, NT, SM::XPT, p->stream>>>(sqrt_d + (size_t)k * nz * NN, sqrt_dref, p->partQ, p->T1, tb,
+                                                        seq, pa, nz, N);
+      k_pag_cols<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T1, p->T3, tb, seq, pa, nz, cden, 1.0f / ((float)L * L));
+      k_pag_final<L><<<L / G, NT, SM::X, p->stream>>>(p->T3, psi0 + (size_t)k * LL, tb, (float)db);
+      pend(p, HOLO_PASS_FILTER, A * (3.0 * nz + 2.0) + 4.0 * NN * (nz + 1), L * fftf(L) * (12.0 * nz + 2.0), 3);
     }
   }
 
@@ -275,6 +313,33 @@ struct RefRun {
     }
   }
 
+  // O17: q0 = mean_r(c_r) + (1/R) sum_r S_{-s_r} P_{-zeta0} Z (a_r - c_r),  c_r = mean(a_r)
+  //      (= (1/R) sum_r S_{-s_r} P_{-zeta0} Z_{c_r} a_r: a constant is invariant under S and P)
+  static void init_probe(holo_plan *p, const float *sqrt_dref, float2 *q0) {
+    const int N = p->N, R = p->n_ref;
+    const size_t SM = E::SMEM, NN = (size_t)N * N;
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
+    const double A = 8.0 * L * L, fl = fftf(L);
+    pbeg(p);
+    k_frame_stats<<<R, 256, 0, p->stream>>>(sqrt_dref, NN, p->partR, nullptr);
+    pend(p, HOLO_PASS_REDUCE, 4.0 * NN * R, 0);
+    for (int r = 0; r < R; r++) {
+      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
+      pbeg(p);
+      k_ref_rows<L, REF_INIT><<<gn, E::NT, SM, p->stream>>>(nullptr, sqrt_dref + r * NN, p->Vr, p->partR + r, Hx, tw,
+                                                              p->tw3, N, 1.f, 0);
+      k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, p->tw3, N, r == 0);
+      pend(p, HOLO_PASS_REF, A * (0.0625 + 0.5 + 0.5 + (r ? 2.0 : 1.0)), fl * (N + L), 2);
+    }
+    pbeg(p);
+    k_fill_mean<<<1184, 256, 0, p->stream>>>(q0, (size_t)L * L, p->partR, R);
+    k_ref_cols<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, p->Ghat, nullptr, tw, p->tw3, N, 0);
+    k_ref_rows<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, nullptr, q0, nullptr, nullptr, tw, p->tw3, N,
+                                                             1.0f / R, 1);
+    pend(p, HOLO_PASS_REF, 6 * A, 2.0 * L * fl, 3);
+  }
+
   static void run(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc) {
     const int N = p->N, R = p->n_ref;
     const size_t SM = E::SMEM;
@@ -325,8 +390,11 @@ struct RefRun {
                                         holo_run::RefRun<LV>::run,                                             \
                                         holo_run::RefRun<LV>::fwd,                                             \
                                         holo_run::Run<LV>::upsample2,                                          \
+                                        holo_run::Run<LV>::init_psi,                                           \
+                                        holo_run::RefRun<LV>::init_probe,                                      \
                                         holo::LineEng<LV>::G};
 #define HOLO_DEFINE_REF_OPS(LV)                                                                                  \
   static void holo_set_attrs_##LV() { holo_run::set_ref_attrs<LV>(); }                                          \
   extern const HoloOps holo_ops_##LV = {LV,      holo_set_attrs_##LV,       nullptr, holo_run::RefRun<LV>::run, \
-                                        holo_run::RefRun<LV>::fwd, nullptr, holo::LineEng<LV>::G};
+                                        holo_run::RefRun<LV>::fwd, nullptr, nullptr,                           \
+                                        holo_run::RefRun<LV>::init_probe, holo::LineEng<LV>::G};

@@ -12,7 +12,7 @@ HDR = os.path.join(ROOT, "include", "holo.h")
 
 def declared():
     txt = open(HDR).read()
-    return sorted(set(re.findall(r"\b(holo_[a-z_]+)\s*\(", txt)) - {"holo_status"})
+    return sorted(set(re.findall(r"\b(holo_[a-z0-9_]+)\s*\(", txt)) - {"holo_status"})
 
 
 def test_header_declares_the_north_star_entry_points():
@@ -25,7 +25,7 @@ def test_header_declares_the_north_star_entry_points():
 def test_library_exports_every_declared_symbol():
     import paper_2407_20304_b200 as hb
     out = subprocess.run(["nm", "-D", "--defined-only", hb.LIB_PATH], capture_output=True, text=True).stdout
-    exported = set(re.findall(r" T (holo_[a-z_]+)", out))
+    exported = set(re.findall(r" T (holo_[a-z0-9_]+)", out))
     missing = [s for s in declared() if s not in exported]
     assert not missing, missing
     assert set(hb.EXPORTED) <= exported
