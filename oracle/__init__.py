@@ -66,6 +66,8 @@ def _load():
         lib.or_upsample2.argtypes = [Ic, P, P]
         lib.or_bin2.argtypes = [Ic, Ic, P, P]
         lib.or_init_probe.argtypes = [Ic, Ic, Ic, D, D, D, P, P, P]
+        lib.or_grad_full.argtypes = geo + [P, P, P, P, Ic, D, P, P, P, P]
+        lib.or_grad_full.restype = D
         lib.or_multipaganin.argtypes = [Ic, Ic, Ic, D, D, P, P, P, P, P, D, P]
         _lib = lib
     return _lib
@@ -251,3 +253,24 @@ def multipaganin(geom: Geometry, L, shifts_k, sqrt_d_k, sqrt_dref, delta_beta):
     _load().or_multipaganin(geom.nz, L, N, geom.wavelength, geom.p0, _p(geom.mt), _p(geom.zeta), _p(sk),
                             _p(sqrt_d_k), _p(sqrt_dref), float(delta_beta), _p(out))
     return out
+
+
+def grad_full(geom: Geometry, psi, q, shifts, pshifts, sqrt_d, ref_shifts=None, sqrt_dref=None,
+              want_psi=True, want_q=True):
+    """O19: F and gradients of the full Eq. (10) objective -- per-frame probe shifts s^p_kj
+    (q_kj = P_omega S_{s^p} q) and, when sqrt_dref is given, the reference term (O14)."""
+    psi = _c(psi, np.complex128)
+    q = _c(q, np.complex128)
+    sqrt_d = _c(sqrt_d, np.float64)
+    K, L = psi.shape[0], psi.shape[1]
+    N = sqrt_d.shape[-1]
+    shifts, ga = _geo_args(geom, K, L, N, shifts)
+    ps = _c(pshifts, np.float64).reshape(K, geom.nz, 2)
+    R = 0 if sqrt_dref is None else sqrt_dref.shape[0]
+    rs = _c(ref_shifts if R else np.zeros((1, 2)), np.float64).reshape(-1, 2)
+    dr = _c(sqrt_dref if R else np.zeros((1, N, N)), np.float64)
+    gp = np.empty_like(psi) if want_psi else None
+    gq = np.empty_like(q) if want_q else None
+    F = _load().or_grad_full(*ga, _p(ps), _p(psi), _p(q), _p(sqrt_d), R, float(geom.zeta[0]), _p(rs), _p(dr),
+                             _p(gp), _p(gq))
+    return F, gp, gq

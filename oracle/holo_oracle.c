@@ -543,3 +543,57 @@ void or_multipaganin(int nz, int L, int N, double lam, double p0, const double *
   }
   free(t); free(num); free(W);
 }
+
+/* ------------------------------------------------------------------ O19 --- */
+/* The full objective of Eq. (10) with per-frame PROBE shifts s^p_kj and the reference term
+ * (Eq. (12)):
+ *   q_kj = P_{omega_j} S_{s^p_kj} q,   w_kj = C P_{zdet_j}( q_kj . M_{1/mt_j} S_{s_kj} psi_k )
+ *   F = sum_kj sum (|w_kj| - a_kj)^2 + F_ref (O14, when R > 0)
+ *   grad_psi_k = 2 sum_j (M S)^*( conj(q_kj) v_kj ),  v = P_{-zdet} Z rho        (L*_kj)
+ *   grad_q     = 2 sum_kj S_{-s^p_kj} P_{-omega_j}( conj(M S psi_k) v_kj ) + O14's term
+ * pshifts [K][nz][2]; ref_shifts [R][2], sqrt_dref [R][N][N] (R = 0: no reference term).
+ * With s^p = 0 this is O8-O12 (+ O14).  Summation: F over j, k, pixels; grad_q over j, k. */
+double or_grad_full(int K, int nz, int L, int N, double lam, double p0, const double *mt, const double *zdet,
+                    const double *omega, const double *shifts, const double *pshifts, const cplx *psi,
+                    const cplx *q, const double *sqrt_d, int R, double zeta0, const double *ref_shifts,
+                    const double *sqrt_dref, cplx *grad_psi, cplx *grad_q) {
+  long LL = (long)L * L, NN = (long)N * N;
+  cplx *qk = (cplx *)malloc(sizeof(cplx) * LL), *a = (cplx *)malloc(sizeof(cplx) * LL);
+  cplx *v = (cplx *)malloc(sizeof(cplx) * LL), *t = (cplx *)malloc(sizeof(cplx) * LL);
+  cplx *w = (cplx *)malloc(sizeof(cplx) * NN);
+  double F = 0;
+  if (grad_psi) memset(grad_psi, 0, sizeof(cplx) * LL * K);
+  if (grad_q) memset(grad_q, 0, sizeof(cplx) * LL);
+  for (int j = 0; j < nz; j++)
+    for (int k = 0; k < K; k++) {
+      const double *s = shifts + ((long)k * nz + j) * 2, *sp = pshifts + ((long)k * nz + j) * 2;
+      const double *d = sqrt_d + ((long)k * nz + j) * NN;
+      or_shift(L, sp[0], sp[1], q, qk);
+      or_prop(L, lam, p0, omega[j], qk, qk);                    /* q_kj = P_omega S_{s^p} q */
+      or_mag(L, mt[j], s[0], s[1], psi + k * LL, a);            /* a = M S psi_k */
+      for (long i = 0; i < LL; i++) t[i] = qk[i] * a[i];
+      or_prop(L, lam, p0, zdet[j], t, t);
+      crop(L, N, t, w);
+      for (long i = 0; i < NN; i++) {
+        double m = cabs(w[i]);
+        F += (m - d[i]) * (m - d[i]);
+        w[i] = m > 0 ? w[i] - d[i] * w[i] / m : 0;
+      }
+      zpad(L, N, w, v);
+      or_prop(L, lam, p0, -zdet[j], v, v);
+      if (grad_q) {
+        for (long i = 0; i < LL; i++) t[i] = conj(a[i]) * v[i];
+        or_prop(L, lam, p0, -omega[j], t, t);
+        or_shift(L, -sp[0], -sp[1], t, t);                     /* Q_kj^* = S_{-s^p} P_{-omega} (.) */
+        for (long i = 0; i < LL; i++) grad_q[i] += 2.0 * t[i];
+      }
+      if (grad_psi) {
+        for (long i = 0; i < LL; i++) t[i] = conj(qk[i]) * v[i];
+        or_mag_adj(L, mt[j], s[0], s[1], t, t);
+        for (long i = 0; i < LL; i++) grad_psi[k * LL + i] += 2.0 * t[i];
+      }
+    }
+  if (R > 0) F += or_grad_ref(R, L, N, lam, p0, zeta0, ref_shifts, q, sqrt_dref, grad_q);
+  free(qk); free(a); free(v); free(t); free(w);
+  return F;
+}

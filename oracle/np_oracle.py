@@ -154,6 +154,35 @@ class Problem:
             gq += 2.0 * prop(G[j], self.g.wavelength, self.g.p0, -self.g.omega[j])
         return F, gpsi, gq
 
+    def qkj(self, q, j, sp):
+        """O19: q_kj = P_{omega_j} S_{s^p_kj} q (Eq. (10), probe shift s^p)."""
+        return prop(shift(q, float(sp[0]), float(sp[1])), self.g.wavelength, self.g.p0, self.g.omega[j])
+
+    def grad_full(self, psi, q, shifts, pshifts, sqrt_d, ref_shifts=None, sqrt_dref=None, tau=1, frames=None):
+        """O19: F, grad_psi, grad_q of Eq. (10) with probe shifts (Q_kj^* = S_{-s^p} P_{-omega} (.)) and,
+        when sqrt_dref is given, the reference term (O14) -- Eq. (12) P:125-129."""
+        K, nz = psi.shape[0], self.g.nz
+        frames = frames if frames is not None else [(k, j) for j in range(nz) for k in range(K)]
+        F = 0.0
+        gpsi = np.zeros_like(psi, dtype=np.complex128)
+        gq = np.zeros((self.L, self.L), np.complex128)
+        for (k, j) in frames:
+            sp = pshifts[k, j]
+            Fk, gk, Gk = self.frame_grad(psi[k], self.qkj(q, j, sp), j, shifts[k, j], sqrt_d[k, j], tau)
+            F += Fk
+            gpsi[k] += gk
+            gq += 2.0 * shift(prop(Gk, self.g.wavelength, self.g.p0, -self.g.omega[j]), -float(sp[0]), -float(sp[1]))
+        if sqrt_dref is not None:
+            Fr, gr = grad_ref(self.g.wavelength, self.g.p0, self.g.zeta[0], q, ref_shifts, sqrt_dref, tau=tau)
+            F += Fr
+            gq += gr
+        return F, gpsi, gq
+
+    def fwd_full(self, psi, q, shifts, pshifts):
+        K, nz = psi.shape[0], self.g.nz
+        return {(k, j): self.frame_fwd(psi[k], self.qkj(q, j, pshifts[k, j]), j, shifts[k, j])[0]
+                for k in range(K) for j in range(nz)}
+
     def fwd(self, psi, q, shifts, frames=None):
         K, nz = psi.shape[0], self.g.nz
         frames = frames if frames is not None else [(k, j) for k in range(K) for j in range(nz)]
