@@ -313,6 +313,53 @@ def run_reference_ref_arm(args, cfg, g, npo):
                       "vs_baseline": None}))
 
 
+def run_multires(args, cfg, hb, dev, local, k0):
+    """3-level schedule [(4, it), (2, it), (1, it)] through multires.run_schedule on K angles of the
+    workload: data = |holo_fwd(truth)| + Poisson at full resolution, binned on the GPU per level;
+    initial guess psi = 1, q = 0.9 x the 4x4 block mean of the true probe.  Per-level CUDA-event times."""
+    from paper_2407_20304_b200 import multires
+    K, it = args.multires_angles, args.multires_iters
+    plan = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=local,
+                   angle_batch=min(args.batch, K))
+    s = synth.shifts(cfg)[k0:k0 + K]
+    plan.set_shifts(s)
+    q_t = synth.probe(cfg, device=dev, dtype=torch.complex64)
+    psi_t = synth.psi_stack(cfg, K=K, device=dev, dtype=torch.complex64, k0=k0)
+    w = torch.empty(K, cfg.nz, cfg.n, cfg.n, dtype=torch.complex64, device=dev)
+    plan.fwd(psi_t, q_t, w)
+    sqrt_d = synth.poisson_amplitude(w.abs().square_(), cfg.photons, cfg, item=99).float().contiguous()
+    del w, psi_t, plan
+    f0 = 4
+    Lc = cfg.npad // f0
+    q0 = (0.9 * q_t.reshape(Lc, f0, Lc, f0).mean(dim=(1, 3))).contiguous()
+    psi0 = torch.ones(K, Lc, Lc, dtype=torch.complex64, device=dev)
+    levels = [(4, it), (2, it), (1, it)]
+    marks = []
+
+    def on_level(h):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        marks.append((h, e))
+
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    multires.run_schedule(levels, sqrt_d, s, cfg.n, cfg.npad, cfg.z1, cfg.wavelength, cfg.Z, cfg.det_pixel, psi0, q0,
+                          rho_q=1.0 / K, device=local, angle_batch=min(args.batch, K), on_level=on_level)
+    torch.cuda.synchronize()
+    out, prev = [], e0
+    for (h, e) in marks:
+        ms = prev.elapsed_time(e)
+        f = h["factor"]
+        frames = K * cfg.nz * h["iterations"]
+        out.append({"factor": f, "npad": cfg.npad // f, "n": cfg.n // f, "iterations": h["iterations"],
+                    "sweeps": h["sweeps"], "F_start": h["F_start"], "F_end": h["F_end"], "ms": ms,
+                    "frame_it_per_s": frames / (ms / 1e3)})
+        prev = e
+    return {"angles": K, "levels": out, "total_ms": e0.elapsed_time(prev),
+            "note": "each level's ms includes its plan creation, data binning, upsampling and CG iterations"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -325,6 +372,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rho-q", type=float, default=None)
     ap.add_argument("--batch", type=int, default=8, help="angle_batch of the plan (angles per Y1/X2/Y2 launch)")
+    ap.add_argument("--multires-angles", type=int, default=16,
+                    help="angles of the timed 3-level multiresolution run (SURVEY 8(f) row 3); 0 = skip")
+    ap.add_argument("--multires-iters", type=int, default=3, help="CG iterations per level of that run")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -509,6 +559,15 @@ def main():
                "steps": ns}
         del host_d
 
+    # ---- the multiresolution schedule: 3 levels (4x4, 2x2, 1x1 binning)
+    #      of the same workload on a smaller angle set, timed with CUDA events per level (a separate
+    #      run after the headline measurement, its own memory: the main solver is released first)
+    multires = None
+    if args.multires_angles > 0 and cfg.name != "cfg4":
+        del solver, plan, sqrt_d
+        torch.cuda.empty_cache()
+        multires = run_multires(args, cfg, hb, dev, local, k0)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_ref(cfg) if cfg.name == "cfg4" else cpu_baseline(cfg)
@@ -525,7 +584,7 @@ def main():
             "roofline_step": step, "fp32_peak": fp,
             "profiled_steps_overhead": prof_overhead,
             "roofline": roof, "passes": passes, "gpu_launches": int(launches),
-            "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu,
+            "clocks": clocks, "e2e": e2e, "cpu_baseline": cpu, "multires": multires,
         }
         print(json.dumps(out))
     if world > 1:

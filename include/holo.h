@@ -90,6 +90,16 @@ holo_status holo_plan_derived(const holo_plan *p, double *m0, double *mt, double
  * Copied into the plan (the host buffer may be reused on return).  Default: all zero. */
 holo_status holo_set_shifts(holo_plan *p, const double *s /*[host]*/);
 
+/* Per-frame PROBE shifts s^p_kj (Eq. (9)/(10) P:108, "S_{s^p_{k,j}}"; O19):
+ * [host] float64 [n_angles][nz][2] = (sx, sy) in psi-grid pixels, |s| < npad/2.  After this call
+ * every sweep of the object chain (holo_fwd / holo_adj / holo_grad / holo_grad_full) uses
+ *   q_kj = P_{omega_j} S_{s^p_kj} q  instead of  q_j = P_{omega_j} q,
+ * and the probe gradient 2 sum_kj S_{-s^p_kj} P_{-omega_j}(conj(M S psi_k) v_kj) is accumulated in the
+ * Fourier domain (two extra row passes per angle, one extra transform per frame in Y1 and Y2).
+ * The first call allocates the path's workspace (~ (2 nz + 1) angle_batch + 2 complex64 npad^2 arrays);
+ * a NULL s switches the path off again (plain q_j).  Power-of-two npad, n_angles > 0. */
+holo_status holo_set_probe_shifts(holo_plan *p, const double *s /*[host] | NULL*/);
+
 /* Reference-frame shifts s^r_r (Eq. (10) reference term P:115; reading C16):
  * [host] float64 [n_ref][2] = (sx, sy).  Sets R = n_ref for holo_grad_ref. */
 holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s /*[host]*/);
@@ -122,6 +132,17 @@ holo_status holo_adj(holo_plan *p, const void *y /*[K][nz][n][n]*/, const void *
  * grad_psi / grad_q_part may be NULL (not computed).  sqrt_d: float32 [K][nz][n][n] >= 0. */
 holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float *sqrt_d,
                       const void *eta_psi_prev, void *grad_psi, void *grad_q_part, double *sc, uint32_t flags);
+
+/* The complete Eq. (10) objective in ONE sweep (O19; Eq. (12)): the object
+ * chain of holo_grad (with the probe shifts of holo_set_probe_shifts, if set) PLUS the n_ref
+ * reference frames sqrt_dref [R][n][n] (holo_set_ref_shifts), sharing DFT2(q) and the
+ * Fourier-domain probe-gradient accumulator:
+ *   sc[0] = F_local + F_ref,  sc[1], sc[2] as holo_grad,
+ *   grad_q_part = 2 sum_kj Q_kj^*(rho_kj) + 2 sum_r Q_r^*(rho^r)   (local partial).
+ * sqrt_dref may be NULL (then identical to holo_grad).  Flags as holo_grad. */
+holo_status holo_grad_full(holo_plan *p, const void *psi, const void *q, const float *sqrt_d,
+                           const float *sqrt_dref, const void *eta_psi_prev, void *grad_psi, void *grad_q_part,
+                           double *sc, uint32_t flags);
 
 /* Reference arm (O14; reference constraint P:102, Eq. (10)/(12) reference terms):
  *   sc[0] = F_ref = sum_r sum_pix (|C P_{zeta0} S_{s_r} q| - sqrt_dref_r)^2
@@ -208,7 +229,8 @@ uint64_t holo_launch_count(const holo_plan *p);
 #define HOLO_PASS_REDUCE 6
 #define HOLO_PASS_CG 7
 #define HOLO_PASS_REF 8
-#define HOLO_NPASS 9
+#define HOLO_PASS_PS 9 /* probe-shift passes XQ / XG (holo_set_probe_shifts) */
+#define HOLO_NPASS 10
 holo_status holo_profile_enable(holo_plan *p, int enable);
 holo_status holo_profile_read(holo_plan *p, double *ms, uint64_t *launches, double *bytes, double *flops, int reset);
 

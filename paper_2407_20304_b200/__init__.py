@@ -92,20 +92,26 @@ _lib.holo_init_probe.restype = _S
 _lib.holo_init_psi.argtypes = [_P, _P, _P, ctypes.c_double, _P]
 _lib.holo_init_psi.restype = _S
 
+_lib.holo_set_probe_shifts.argtypes = [_P, _P]
+_lib.holo_set_probe_shifts.restype = _S
+_lib.holo_grad_full.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_uint32]
+_lib.holo_grad_full.restype = _S
+
 _lib.holo_profile_enable.argtypes = [_P, ctypes.c_int]
 _lib.holo_profile_enable.restype = _S
 _lib.holo_profile_read.argtypes = [_P, _P, _P, _P, _P, ctypes.c_int]
 _lib.holo_profile_read.restype = _S
 
-HOLO_NPASS = 9
-PASS_NAMES = ["X1", "Y1", "X2", "Y2", "X3", "filter", "reduce", "cg", "ref"]
+HOLO_NPASS = 10
+PASS_NAMES = ["X1", "Y1", "X2", "Y2", "X3", "filter", "reduce", "cg", "ref", "ps"]
 PASS_KERNELS = ["k_x1", "k_y1", "k_x2", "k_y2", "k_x3", "k_rows_filter|k_cols_filter|k_p2_convert",
-                "k_reduce|k_dots", "k_cg", "k_ref"]
+                "k_reduce|k_dots", "k_cg", "k_ref", "k_xq|k_xg"]
 
 EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes", "holo_last_error",
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
             "holo_grad_ref", "holo_fwd_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
-            "holo_profile_read", "holo_upsample2", "holo_bin2", "holo_init_probe", "holo_init_psi"]
+            "holo_profile_read", "holo_upsample2", "holo_bin2", "holo_init_probe", "holo_init_psi",
+            "holo_set_probe_shifts", "holo_grad_full"]
 
 
 class HoloError(RuntimeError):
@@ -201,6 +207,14 @@ class Plan:
         s = np.ascontiguousarray(s, dtype=np.float64).reshape(self.K, self.nz, 2)
         self._chk(_lib.holo_set_shifts(self._h, s.ctypes.data_as(_P)))
 
+    def set_probe_shifts(self, s):
+        """holo_set_probe_shifts: per-frame probe shifts s^p [K][nz][2] (None: plain q_j path)."""
+        if s is None:
+            self._chk(_lib.holo_set_probe_shifts(self._h, None))
+            return
+        s = np.ascontiguousarray(s, dtype=np.float64).reshape(self.K, self.nz, 2)
+        self._chk(_lib.holo_set_probe_shifts(self._h, s.ctypes.data_as(_P)))
+
     def set_ref_shifts(self, s):
         s = np.ascontiguousarray(s, dtype=np.float64).reshape(-1, 2)
         self._chk(_lib.holo_set_ref_shifts(self._h, s.shape[0], s.ctypes.data_as(_P)))
@@ -230,6 +244,18 @@ class Plan:
                                  _ptr(grad_psi, torch.complex64, self.K * LL, "grad_psi"),
                                  _ptr(grad_q_part, torch.complex64, LL, "grad_q_part"),
                                  _ptr(sc, torch.float64, 3, "sc"), flags))
+
+    def grad_full(self, psi, q, sqrt_d, sqrt_dref, sc, eta_psi_prev=None, grad_psi=None, grad_q_part=None, flags=0):
+        """holo_grad_full: the object chain and the n_ref reference frames in one sweep (Eq. (10)/(12))."""
+        LL, NN = self.npad ** 2, self.n ** 2
+        self._chk(_lib.holo_grad_full(self._h, _ptr(psi, torch.complex64, self.K * LL, "psi"),
+                                      _ptr(q, torch.complex64, LL, "q"),
+                                      _ptr(sqrt_d, torch.float32, self.K * self.nz * NN, "sqrt_d"),
+                                      _ptr(sqrt_dref, torch.float32, self.n_ref * NN, "sqrt_dref"),
+                                      _ptr(eta_psi_prev, torch.complex64, self.K * LL, "eta_psi_prev"),
+                                      _ptr(grad_psi, torch.complex64, self.K * LL, "grad_psi"),
+                                      _ptr(grad_q_part, torch.complex64, LL, "grad_q_part"),
+                                      _ptr(sc, torch.float64, 3, "sc"), flags))
 
     def grad_ref(self, q, sqrt_dref, sc, grad_q_part=None, flags=0):
         self._chk(_lib.holo_grad_ref(self._h, _ptr(q, torch.complex64, self.npad ** 2, "q"),

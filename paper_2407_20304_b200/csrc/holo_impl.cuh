@@ -51,6 +51,10 @@ struct holo_plan {
   // initial object (O18, holo_init.cuh): inverse-magnification Bluestein tables [nz][L] (mt' = 1/mt_j)
   float2 *pcin = nullptr, *pcout = nullptr, *pbke = nullptr, *pbko = nullptr;
   std::vector<double> shifts_host;  // [K][nz][2] as last set by holo_set_shifts
+  // per-frame probe shifts (O19, holo_set_probe_shifts): Hq [K][nz][2][L] = h_omega_j r_{s^p_kj} / L per axis;
+  // Qt [B][nz][L][L] (IDFT_x(Hq_x Qhat), P2), Qk [B][L][L] (q_kj, P2), Ut [B][nz][L][L] (probe-gradient terms)
+  bool ps = false;
+  float2 *hq = nullptr, *Qt = nullptr, *Qk = nullptr, *Ut = nullptr;
   // per-pass event profiling (holo_profile_*)
   struct Rec {
     int id;
@@ -84,7 +88,8 @@ struct HoloOps {
   void (*set_attrs)();
   // mode: 0 grad, 1 fwd, 2 adj (y given), 3 objective only
   void (*sweep)(holo_plan *p, int mode, const float2 *psi, const float2 *q, const float *sqrt_d, const float2 *yin,
-                float2 *wout, const float2 *eta, float2 *gpsi, float2 *gq_out, float gscale, bool want_q, bool acc_q);
+                float2 *wout, const float2 *eta, float2 *gpsi, float2 *gq_out, float gscale, bool want_q, bool acc_q,
+                const float *sqrt_dref);
   void (*ref_run)(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc);
   void (*ref_fwd)(holo_plan *p, const float2 *q, float2 *w);
   void (*upsample2)(holo_plan *p, const float2 *coarse, float2 *fine, int count);  // NULL: unsupported L

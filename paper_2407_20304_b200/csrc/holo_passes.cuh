@@ -109,8 +109,12 @@ __global__ void __launch_bounds__(NT, 1)
 //            W1[b] = rows [o, o+N) of D_y(q_j . a) (optional; P2 with N rows)
 // The frame body is a separate (non-inlined) function: only the loop state crosses the
 // call, so the transforms keep the full register budget (an inlined loop spills).
-template <int L>
+// PS (per-frame probe shifts): q_kj = P_omega S_{s^p} q is not a
+// per-plane constant; its column comes from qt = IDFT_x(Hq_x Qhat) (XQ pass, spectral in y):
+// x Hq_y (table), IFFT_y -> q_kj column, stored to qk (Y2 needs conj(q_kj)).
+template <int L, bool PS>
 __device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float2 *__restrict__ qj,
+                                      const float2 *__restrict__ qt, float2 *__restrict__ qk,
                                       float2 *__restrict__ aout, float2 *__restrict__ w1, const float4 *__restrict__ tw,
                                       const TabSeq &seq, TabPipe<L> &pipe, float2 *sm, int mag, int N) {
   using C = CtaK<L>;
@@ -134,9 +138,24 @@ __device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float
     fft<L, true>(v, x, t, tw);
   }
   if (aout) st_p2_col<L>(v, aout, col, L, t);
-  if (w1) {
+  if (PS && qk) {  // q_kj column: park a, transform the qt column
+#pragma unroll
+    for (int r = 0; r < 16; r++) X[r] = v[r];
+    ld_p2_col<L>(v, qt, col, L, t);
+    const float2 *hq = pipe.take(seq);  // Hq_y(k, j) = h_omega r_{s^p_y} / L
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmul(v[r], hq[t + r * T]);
+    fft<L, true>(v, x, t, tw);
+    st_p2_col<L>(v, qk, col, L, t);
+    if (w1) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cmul(v[r], X[r]);
+    }
+  } else if (w1) {
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + p2(t + r * T, col, L)));
+  }
+  if (w1) {
     fft<L, false>(v, x, t, tw);
     const float2 *h = pipe.take(seq);  // hdet_j / L
 #pragma unroll
@@ -151,10 +170,11 @@ __device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float
   }
 }
 
-template <int L>
+template <int L, bool PS>
 __global__ void __launch_bounds__(NT, 1)
-    k_y1(const float2 *__restrict__ T1j, size_t fstride, const float2 *__restrict__ qj, float2 *__restrict__ Aout,
-         float2 *__restrict__ W1, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
+    k_y1(const float2 *__restrict__ T1j, size_t fstride, const float2 *__restrict__ qj, const float2 *__restrict__ Qt,
+         float2 *__restrict__ Qk, float2 *__restrict__ Aout, float2 *__restrict__ W1, Tables tb,
+         const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
   using C = CtaK<L>;
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
@@ -166,8 +186,9 @@ __global__ void __launch_bounds__(NT, 1)
   for (int b = 0; b < nb; b++) {
     const float2 *in = T1j + (size_t)b * fstride;
     if (threadIdx.x == 0 && b + 1 < nb) prefetch_l2(in + fstride + p2(0, col0, L), 8u * C::G * L);
-    y1_frame<L>(in, qj, Aout ? Aout + (size_t)b * L * L : nullptr, W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq,
-                pipe, sm, mag, N);
+    y1_frame<L, PS>(in, qj, PS ? Qt + (size_t)b * fstride : nullptr, (PS && Qk) ? Qk + (size_t)b * L * L : nullptr,
+                    Aout ? Aout + (size_t)b * L * L : nullptr, W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq, pipe,
+                    sm, mag, N);
   }
 }
 
@@ -273,11 +294,14 @@ __global__ void __launch_bounds__(NT, 1)
 // read-modify-written once per frame by the SAME CTA for its columns, so across the
 // batch it stays in L2 (DRAM sees ~one read + one write per batch).
 // Per frame:  v = D_y^* pad(V1 col);  G_j += conj(a) v;  T3j = (M S)_y^*(conj(q_j) v)
-template <int L>
+// PS: instead of G_j += conj(a) v, the frame's probe-gradient term u = conj(a) v is taken to
+// the y-spectrum with conj(Hq_y) and stored to ut (XG finishes the x axis and accumulates
+// the Fourier-domain sum, Eq. (12) with Q_kj^* = S_{-s^p} P_{-omega}); conj(q_kj) comes from qk.
+template <int L, bool PS>
 __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const float2 *__restrict__ ab,
-                                      const float2 *__restrict__ qj, float2 *__restrict__ Gj, float2 *__restrict__ t3,
-                                      const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> &pipe, float2 *sm,
-                                      int mag, int N) {
+                                      const float2 *__restrict__ qj, float2 *__restrict__ Gj, float2 *__restrict__ ut,
+                                      float2 *__restrict__ t3, const float4 *__restrict__ tw, const TabSeq &seq,
+                                      TabPipe<L> &pipe, float2 *sm, int mag, int N) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   Xch x = C::xch(sm);
@@ -297,7 +321,20 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], h[t + r * T]);
   }
   fft<L, true>(v, x, t, tw);
-  if (Gj) {
+  if (PS && ut) {
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      Y[r] = v[r];
+      v[r] = cmulc(v[r], ldg2(ab + p2(t + r * T, col, L)));  // conj(a) v
+    }
+    fft<L, false>(v, x, t, tw);
+    const float2 *hq = pipe.take(seq);  // Hq_y(k, j), conjugated
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], hq[t + r * T]);
+    st_p2_col<L>(v, ut, col, L, t);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = Y[r];
+  } else if (Gj) {
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const size_t gi = p2(t + r * T, col, L);
@@ -306,7 +343,7 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
   }
   if (!t3) return;
 #pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));
+  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));  // qj: q_j, or q_kj (PS)
   if (mag) {
 #pragma unroll
     for (int r = 0; r < 16; r++) Y[r] = v[r];
@@ -323,11 +360,11 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
   st_p2_col<L>(v, t3, col, L, t);
 }
 
-template <int L>
+template <int L, bool PS>
 __global__ void __launch_bounds__(NT, 1)
     k_y2(const float2 *__restrict__ V1, const float2 *__restrict__ a, const float2 *__restrict__ qj,
-         float2 *__restrict__ Gj, float2 *__restrict__ T3j, size_t fstride, Tables tb,
-         const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
+         const float2 *__restrict__ Qk, float2 *__restrict__ Gj, float2 *__restrict__ Ut, float2 *__restrict__ T3j,
+         size_t fstride, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
   using C = CtaK<L>;
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
@@ -335,15 +372,17 @@ __global__ void __launch_bounds__(NT, 1)
   TabPipe<L> pipe;
   pipe.start(seq, slot_base<L, true>(sm), bars);
   const int col0 = blockIdx.x * C::G;
+  const bool wq = PS ? Ut != nullptr : Gj != nullptr;
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *vin = V1 + (size_t)b * N * L;
     const float2 *ab = a + (size_t)b * L * L;
     if (threadIdx.x == 0 && b + 1 < nb) {
       prefetch_l2(vin + (size_t)N * L + p2(0, col0, N), 8u * C::G * N);
-      if (Gj) prefetch_l2(ab + (size_t)L * L + p2(0, col0, L), 8u * C::G * L);
+      if (wq) prefetch_l2(ab + (size_t)L * L + p2(0, col0, L), 8u * C::G * L);
     }
-    y2_frame<L>(vin, ab, qj, Gj, T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N);
+    y2_frame<L, PS>(vin, ab, PS ? Qk + (size_t)b * L * L : qj, Gj, (PS && Ut) ? Ut + (size_t)b * fstride : nullptr,
+                    T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N);
   }
 }
 
@@ -427,6 +466,75 @@ __global__ void __launch_bounds__(NT, 1)
   if (threadIdx.x == 0) {
     partial[2 * blockIdx.x] = s0;
     partial[2 * blockIdx.x + 1] = s1;
+  }
+}
+
+// ----------------------------------------------------------------------------- XQ, XG (PS)
+// Per-frame probe shifts (O19): with Qhat = DFT2 q (P2 [fy][fx]) and Hq(k,j) = h_omega_j r_{s^p_kj} / L
+// per axis, q_kj = IDFT_y(Hq_y IDFT_x(Hq_x Qhat)).
+// XQ (rows fy, one angle): Qt_j row = IFFT_x(Hq_x(k, j) Qhat row) for every plane j   (P2 [fy][x])
+template <int L>
+__global__ void __launch_bounds__(NT, 1)
+    k_xq(const float2 *__restrict__ Qhat, float2 *__restrict__ Qt, Tables tb, const __grid_constant__ TabSeq seq,
+         int nz) {
+  using C = CtaK<L>;
+  constexpr int T = L / 16;
+  extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const Priv<NT> X{priv_base<L>(sm)};
+  TabPipe<L> pipe;
+  pipe.start(seq, slot_base<L, true>(sm), bars);
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  {
+    float2 v[16];
+    ld_p2_row<L>(v, Qhat, y, L, t);
+#pragma unroll
+    for (int r = 0; r < 16; r++) X[r] = v[r];
+  }
+#pragma unroll 1
+  for (int j = 0; j < nz; j++) {
+    float2 v[16];
+    const float2 *hq = pipe.take(seq, j > 0);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmul(X[r], hq[t + r * T]);
+    fft<L, true>(v, x, t, tb.tw);
+    st_p2_row<L>(v, Qt + (size_t)j * L * L, y, L, t);
+  }
+}
+
+// XG (rows fy, one angle): Ghat row (+)= sum_j conj(Hq_x(k, j)) FFT_x(Ut_j row)   (first: overwrite)
+template <int L>
+__global__ void __launch_bounds__(NT, 1)
+    k_xg(const float2 *__restrict__ Ut, float2 *__restrict__ Ghat, Tables tb, const __grid_constant__ TabSeq seq,
+         int nz, int first) {
+  using C = CtaK<L>;
+  constexpr int T = L / 16;
+  extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  const Priv<NT> S{priv_base<L>(sm)};
+  TabPipe<L> pipe;
+  pipe.start(seq, slot_base<L, true>(sm), bars);
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+#pragma unroll 1
+  for (int j = 0; j < nz; j++) {
+    float2 v[16];
+    ld_p2_row<L>(v, Ut + (size_t)j * L * L, y, L, t);
+    fft<L, false>(v, x, t, tb.tw);
+    const float2 *hq = pipe.take(seq);
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const float2 a = cmulc(v[r], hq[t + r * T]);
+      S[r] = j == 0 ? a : cadd(S[r], a);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const size_t gi = p2(y, t + r * T, L);
+    Ghat[gi] = first ? S[r] : cadd(Ghat[gi], S[r]);
   }
 }
 

@@ -194,6 +194,8 @@ holo_status upload_cr(holo_plan *p, const double *s) {
   return HOLO_OK;
 }
 
+holo_status ensure_fourier_ws(holo_plan *p);  // below
+
 holo_status precheck(holo_plan *p) {
   if (!p) return HOLO_EINVAL;
   if (p->sticky) return fail(p, HOLO_ESTATE, "plan is in an error state: " + p->err);
@@ -412,14 +414,9 @@ holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
     if (!std::isfinite(s[i]) || std::fabs(s[i]) >= p->L / 2) return fail(p, HOLO_EINVAL, "shift not finite or >= npad/2");
   const int L = p->L, N = p->N;
   const size_t LL = (size_t)L * L;
-  // workspace of the reference arm, allocated on first use
-  if (!p->Qhat) {
-    st = dalloc(p, &p->Qhat, sizeof(float2) * LL);
-    if (st == HOLO_OK) st = dalloc(p, &p->Ghat, sizeof(float2) * LL);
-    if (st == HOLO_OK) st = dalloc(p, &p->Wr, sizeof(float2) * (size_t)N * L);
-    if (st == HOLO_OK) st = dalloc(p, &p->Vr, sizeof(float2) * (size_t)N * L);
-    if (st != HOLO_OK) return st;
-  }
+  // workspace of the reference arm, allocated on first use (shared with the probe-shift path)
+  st = ensure_fourier_ws(p);
+  if (st != HOLO_OK) return st;
   if (n_ref > p->ref_cap) {  // (re)size the per-frame tables; the old ones are freed, not leaked
     const int G = p->ops->ref_lines_per_cta;
     const int nbr = (N + G - 1) / G;  // CTAs of one frame's R2 row pass (one F partial each)
@@ -455,7 +452,7 @@ holo_status holo_fwd(holo_plan *p, const void *psi, const void *q, void *w) {
   if (!psi || !q || !w) return fail(p, HOLO_EINVAL, "null pointer");
   if (p->K == 0) return HOLO_OK;
   p->ops->sweep(p, 1, (const float2 *)psi, (const float2 *)q, nullptr, nullptr, (float2 *)w, nullptr, nullptr,
-                nullptr, 1.0f, false, false);
+                nullptr, 1.0f, false, false, nullptr);
   return postcheck(p);
 }
 
@@ -469,35 +466,115 @@ holo_status holo_adj(holo_plan *p, const void *y, const void *psi, const void *q
     return HOLO_OK;
   }
   p->ops->sweep(p, 2, (const float2 *)psi, (const float2 *)q, nullptr, (const float2 *)y, nullptr, nullptr,
-                (float2 *)adj_psi, (float2 *)adj_q, 1.0f, adj_q != nullptr, false);
+                (float2 *)adj_psi, (float2 *)adj_q, 1.0f, adj_q != nullptr, false, nullptr);
   return postcheck(p);
 }
 
-holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float *sqrt_d, const void *eta_psi_prev,
-                      void *grad_psi, void *grad_q_part, double *sc, uint32_t flags) {
-  holo_status st = precheck(p);
-  if (st != HOLO_OK) return st;
+}  // extern "C"
+
+namespace {
+// holo_grad / holo_grad_full: the object chain (+ the fused reference frames when sqrt_dref)
+holo_status grad_impl(holo_plan *p, const void *psi, const void *q, const float *sqrt_d, const float *sqrt_dref,
+                      const void *eta_psi_prev, void *grad_psi, void *grad_q_part, double *sc, uint32_t flags) {
   const int K = p->K, nz = p->nz, N = p->N, L = p->L;
   if (!q || !sc || (K > 0 && (!psi || !sqrt_d))) return fail(p, HOLO_EINVAL, "null pointer");
   const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0, acc = (flags & HOLO_ACCUMULATE_Q) != 0;
+  const bool ref = sqrt_dref != nullptr && p->n_ref > 0;
   p->tau2 = (flags & HOLO_INTENSITY) ? 1 : 0;
   HC(cudaMemsetAsync(sc, 0, 3 * sizeof(double), p->stream));
+  float2 *gq = obj ? nullptr : (float2 *)grad_q_part;
   if (K == 0) {  // empty shard: F = 0 and a zero probe-gradient partial (sums over no angles)
-    if (!obj && grad_q_part && !acc) HC(cudaMemsetAsync(grad_q_part, 0, sizeof(float2) * (size_t)L * L, p->stream));
-    return HOLO_OK;
+    if (gq && !acc) HC(cudaMemsetAsync(gq, 0, sizeof(float2) * (size_t)L * L, p->stream));
+    if (ref) {  // a reference-only shard: the reference arm alone
+      p->ops->ref_run(p, (const float2 *)q, sqrt_dref, gq, sc, true);
+    }
+    return postcheck(p);
   }
   p->ops->sweep(p, obj ? 3 : 0, (const float2 *)psi, (const float2 *)q, sqrt_d, nullptr, nullptr,
-                (const float2 *)eta_psi_prev, obj ? nullptr : (float2 *)grad_psi,
-                obj ? nullptr : (float2 *)grad_q_part, 2.0f, !obj && grad_q_part != nullptr, acc);
+                (const float2 *)eta_psi_prev, obj ? nullptr : (float2 *)grad_psi, gq, 2.0f, gq != nullptr, acc,
+                ref ? sqrt_dref : nullptr);
   pbeg(p);
   k_reduce<<<1, 1024, 0, p->stream>>>(p->partF, (size_t)K * nz * p->nbx2, 1, sc, 0);
   pend(p, HOLO_PASS_REDUCE, 8.0 * K * nz * ((N + 3) / 4), 0);
+  if (ref) {
+    const int G = p->ops->ref_lines_per_cta, gn = (N + G - 1) / G;
+    pbeg(p);
+    k_reduce<<<1, 1024, 0, p->stream>>>(p->partR, (size_t)p->n_ref * gn, 1, sc, 1);
+    pend(p, HOLO_PASS_REDUCE, 8.0 * p->n_ref * gn, 0);
+  }
   if (!obj && grad_psi) {
     pbeg(p);
     k_reduce<<<1, 1024, 0, p->stream>>>(p->partX3, (size_t)K * p->nbx3, 2, sc + 1, 0);
     pend(p, HOLO_PASS_REDUCE, 8.0 * K * L, 0);
   }
   return postcheck(p);
+}
+
+// reference-arm workspace (Qhat, Ghat: P2 L x L; Wr, Vr: P2 N x L), shared with the probe-shift path
+holo_status ensure_fourier_ws(holo_plan *p) {
+  if (p->Qhat) return HOLO_OK;
+  const size_t LL = (size_t)p->L * p->L, NL = (size_t)p->N * p->L;
+  holo_status st = dalloc(p, &p->Qhat, sizeof(float2) * LL);
+  if (st == HOLO_OK) st = dalloc(p, &p->Ghat, sizeof(float2) * LL);
+  if (st == HOLO_OK) st = dalloc(p, &p->Wr, sizeof(float2) * NL);
+  if (st == HOLO_OK) st = dalloc(p, &p->Vr, sizeof(float2) * NL);
+  return st;
+}
+}  // namespace
+
+extern "C" {
+
+holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float *sqrt_d, const void *eta_psi_prev,
+                      void *grad_psi, void *grad_q_part, double *sc, uint32_t flags) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  return grad_impl(p, psi, q, sqrt_d, nullptr, eta_psi_prev, grad_psi, grad_q_part, sc, flags);
+}
+
+holo_status holo_grad_full(holo_plan *p, const void *psi, const void *q, const float *sqrt_d, const float *sqrt_dref,
+                           const void *eta_psi_prev, void *grad_psi, void *grad_q_part, double *sc, uint32_t flags) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  return grad_impl(p, psi, q, sqrt_d, sqrt_dref, eta_psi_prev, grad_psi, grad_q_part, sc, flags);
+}
+
+holo_status holo_set_probe_shifts(holo_plan *p, const double *s) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  const int L = p->L, nz = p->nz, K = p->K;
+  if (!s) {
+    p->ps = false;
+    return HOLO_OK;
+  }
+  if (K == 0 || !p->ops->sweep) return fail(p, HOLO_EUNSUPPORTED, "probe shifts need angles on a power-of-two torus");
+  for (size_t i = 0; i < (size_t)K * nz * 2; i++)
+    if (!std::isfinite(s[i]) || std::fabs(s[i]) >= L / 2) return fail(p, HOLO_EINVAL, "shift not finite or >= npad/2");
+  if (!p->hq) {
+    const size_t LL = (size_t)L * L, Bc = (size_t)p->B;
+    st = ensure_fourier_ws(p);
+    if (st == HOLO_OK) st = dalloc(p, &p->hq, sizeof(float2) * L * 2 * nz * (size_t)K);
+    if (st == HOLO_OK) st = dalloc(p, &p->Qt, sizeof(float2) * LL * nz * Bc);
+    if (st == HOLO_OK) st = dalloc(p, &p->Qk, sizeof(float2) * LL * Bc);
+    if (st == HOLO_OK) st = dalloc(p, &p->Ut, sizeof(float2) * LL * nz * Bc);
+    if (st != HOLO_OK) return st;
+  }
+  // Hq[k][j][ax][f] = h_{omega_j}[f] r_{s^p_kj,ax}[f] / L  (O3 x O4 per axis; the 1/L of the inverse DFT)
+  std::vector<float2> H((size_t)K * nz * 2 * L);
+  for (int j = 0; j < nz; j++) {
+    const auto h = transfer(L, p->g.wavelength, p->p0, p->omega[j]);
+    for (int k = 0; k < K; k++)
+      for (int ax = 0; ax < 2; ax++) {
+        const double sv = s[((size_t)k * nz + j) * 2 + ax];
+        float2 *dst = H.data() + (((size_t)k * nz + j) * 2 + ax) * L;
+        for (int f = 0; f < L; f++) {
+          const cd v = h[f] * expi2pi_frac(-(double)fbar(f, L) * sv / (double)L) / (double)L;
+          dst[f] = make_float2((float)v.real(), (float)v.imag());
+        }
+      }
+  }
+  HC(cudaMemcpy(p->hq, H.data(), H.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  p->ps = true;
+  return HOLO_OK;
 }
 
 holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref, void *grad_q_part, double *sc,

@@ -27,12 +27,16 @@ void set_chain_attrs() {
   using S = Smem<L>;
   auto a = [](const void *f, size_t s) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s); };
   a((const void *)k_x1<L>, S::XPT);
-  a((const void *)k_y1<L>, S::XPT);
+  a((const void *)k_y1<L, false>, S::XPT);
+  a((const void *)k_y1<L, true>, S::XPT);
+  a((const void *)k_xq<L>, S::XPT);
+  a((const void *)k_xg<L>, S::XPT);
   a((const void *)k_x2<L, X2_GRAD>, S::XT);
   a((const void *)k_x2<L, X2_FWD>, S::XT);
   a((const void *)k_x2<L, X2_ADJ>, S::XT);
   a((const void *)k_x2<L, X2_OBJ>, S::XT);
-  a((const void *)k_y2<L>, S::XPT);
+  a((const void *)k_y2<L, false>, S::XPT);
+  a((const void *)k_y2<L, true>, S::XPT);
   a((const void *)k_x3<L>, S::XPT);
   a((const void *)k_rows_filter<L, false, true, false>, S::X);
   a((const void *)k_rows_filter<L, true, false, false>, S::X);
@@ -59,6 +63,9 @@ void set_ref_attrs() {
   a((const void *)k_ref_rows<L, REF_FWD>);
   a((const void *)k_ref_rows<L, REF_INIT>);
 }
+
+template <int L>
+struct RefRun;
 
 // ------------------------------------------------------------------ object chain
 template <int L>
@@ -150,21 +157,32 @@ struct Run {
     }
   }
 
-  // mode: 0 grad, 1 fwd, 2 adj (y given), 3 objective only
+  // mode: 0 grad, 1 fwd, 2 adj (y given), 3 objective only.
+  // With per-frame probe shifts (p->ps, O19) the probe enters through Qhat = DFT2 q (XQ -> Qt ->
+  // q_kj in Y1) and the probe gradient is accumulated in the Fourier domain (Y2 -> Ut -> XG ->
+  // Ghat); `sqrt_dref` != NULL adds the reference frames (O14) to F and to the same Ghat /
+  // g_q in this call (the fused Eq. (10)/(12)); F partials of those frames go to partR.
   static void sweep(holo_plan *p, int mode, const float2 *psi, const float2 *q, const float *sqrt_d,
                     const float2 *yin, float2 *wout, const float2 *eta, float2 *gpsi, float2 *gq_out, float gscale,
-                    bool want_q, bool acc_q) {
+                    bool want_q, bool acc_q, const float *sqrt_dref) {
     Tables tb = p->tables();
+    const bool ps = p->ps;
     const int N = p->N, nz = p->nz, K = p->K;
     const size_t LL = (size_t)L * L, NL = (size_t)N * L, NN = (size_t)N * N;
     const int nbx2 = p->nbx2;
     const double fl = fftf(L), rN = (double)N / L, NN8 = 8.0 * N * N;
+    const bool gq_pass = want_q && (mode == 0 || mode == 2);
     int nmag = 0;
     for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
-    qj(p, q);
-    if (want_q) cudaMemsetAsync(p->G, 0, sizeof(float2) * LL * nz, p->stream);
+    if (ps) {
+      RefRun<L>::qhat(p, q);
+    } else {
+      qj(p, q);
+      if (want_q) cudaMemsetAsync(p->G, 0, sizeof(float2) * LL * nz, p->stream);
+    }
     // table sequences of the pipelined pointwise steps (holo_kernels.cuh, TabPipe)
     auto crp = [&](int k, int j, int ax) { return p->cr + ((size_t)(k * nz + j) * 2 + ax) * L; };
+    auto hqp = [&](int k, int j, int ax) { return p->hq + ((size_t)(k * nz + j) * 2 + ax) * L; };
     auto add_fwd = [&](TabSeq &q, int k, int j, int ax) {  // mag_fwd: cr, bke, cr, bko, cout
       const float2 *c = crp(k, j, ax);
       const float2 *list[5] = {c, p->bke + (size_t)j * L, c, p->bko + (size_t)j * L, p->cout + (size_t)j * L};
@@ -175,10 +193,10 @@ struct Run {
       const float2 *list[5] = {c, p->bke + (size_t)j * L, c, p->bko + (size_t)j * L, crp(k, j, ax)};
       for (auto *e : list) q.p[q.n++] = e;
     };
-    const bool need_fwd_chain = (mode != 2) || want_q;
+    const bool need_fwd_chain = (mode != 2) || want_q || ps;
     for (int k0 = 0; k0 < K; k0 += p->B) {
       const int nb = K - k0 < p->B ? K - k0 : p->B;  // ragged last batch
-      // ---- X1 (per angle): T1[b][j] = (M S)_x psi_k rows
+      // ---- X1 (per angle): T1[b][j] = (M S)_x psi_k rows;  PS: XQ, Qt[b][j] = IFFT_x(Hq_x Qhat)
       if (need_fwd_chain) {
         for (int b = 0; b < nb; b++) {
           const int k = k0 + b;
@@ -193,12 +211,19 @@ struct Run {
           k_x1<L><<<L / G, NT, SM::XPT, p->stream>>>(psi + (size_t)k * LL, p->T1 + (size_t)b * nz * LL, tb, q, nz,
                                                       p->magmask);
           pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * (1 + 4 * nmag + (nz - nmag)));
+          if (ps) {
+            TabSeq qq{};
+            for (int j = 0; j < nz; j++) qq.p[qq.n++] = hqp(k, j, 0);
+            pbeg(p);
+            k_xq<L><<<L / G, NT, SM::XPT, p->stream>>>(p->Qhat, p->Qt + (size_t)b * nz * LL, tb, qq, nz);
+            pend(p, HOLO_PASS_PS, (1 + nz) * A, L * fl * nz);
+          }
         }
       }
       for (int j = 0; j < nz; j++) {
         const int mag = (p->magmask >> j) & 1;
-        const float2 *qjj = p->QJ + (size_t)j * LL;
-        // ---- Y1 (batched): Aw[b] = (M S)_y T1[b][j];  W1[b] = crop_y D_y (q_j Aw[b])
+        const float2 *qjj = ps ? nullptr : p->QJ + (size_t)j * LL;
+        // ---- Y1 (batched): Aw[b] = (M S)_y T1[b][j];  W1[b] = crop_y D_y (q_(k)j Aw[b])
         if (need_fwd_chain) {
           float2 *aout = want_q ? p->Aw : nullptr;
           float2 *w1 = (mode == 2) ? nullptr : p->W1;
@@ -208,14 +233,21 @@ struct Run {
               add_fwd(q, k0 + b, j, 1);
             else
               q.p[q.n++] = crp(k0 + b, j, 1);
+            if (ps) q.p[q.n++] = hqp(k0 + b, j, 1);
             if (w1) q.p[q.n++] = p->hdet + (size_t)j * L;
           }
           pbeg(p);
-          k_y1<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T1 + (size_t)j * LL, (size_t)nz * LL, qjj, aout, w1, tb, q,
-                                                      mag, N, nb);
-          // bytes: T1 read, Aw write, W1 write per frame; q_j once per batch (L2-resident)
-          pend(p, HOLO_PASS_Y1, nb * (A + (w1 ? rN * A : 0) + (aout ? A : 0)) + (w1 ? A : 0),
-               nb * L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0)));
+          if (ps)
+            k_y1<L, true><<<L / G, NT, SM::XPT, p->stream>>>(p->T1 + (size_t)j * LL, (size_t)nz * LL, nullptr,
+                                                              p->Qt + (size_t)j * LL, p->Qk, aout, w1, tb, q, mag, N,
+                                                              nb);
+          else
+            k_y1<L, false><<<L / G, NT, SM::XPT, p->stream>>>(p->T1 + (size_t)j * LL, (size_t)nz * LL, qjj, nullptr,
+                                                               nullptr, aout, w1, tb, q, mag, N, nb);
+          // bytes: T1 read, Aw write, W1 write per frame; q_j once per batch (L2-resident); PS: Qt read, Qk write
+          pend(p, HOLO_PASS_Y1,
+               nb * (A + (w1 ? rN * A : 0) + (aout ? A : 0) + (ps ? 2 * A : 0)) + ((w1 && !ps) ? A : 0),
+               nb * L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0) + (ps ? 1 : 0)));
         }
         // ---- X2 (batched over blockIdx.y)
         double *pf = p->partF + ((size_t)k0 * nz + j) * nbx2;
@@ -246,12 +278,15 @@ struct Run {
                                                          nz * nbx2, tb, qh, N, p->tau2);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
         }
-        // ---- Y2 (batched): v = D_y^* V1[b]; G_j += conj(Aw[b]) v; T3[b][j] = (M S)_y^* (conj(q_j) v)
-        float2 *Gj = want_q ? p->G + (size_t)j * LL : nullptr;
+        // ---- Y2 (batched): v = D_y^* V1[b]; G_j += conj(Aw[b]) v  (PS: Ut[b][j] = Hq_y^* FFT_y(conj(Aw) v));
+        //      T3[b][j] = (M S)_y^* (conj(q_(k)j) v)
+        float2 *Gj = (want_q && !ps) ? p->G + (size_t)j * LL : nullptr;
+        float2 *Utj = (want_q && ps) ? p->Ut + (size_t)j * LL : nullptr;
         float2 *T3j = gpsi ? p->T3 + (size_t)j * LL : nullptr;
         TabSeq q2{};
         for (int b = 0; b < nb; b++) {
           q2.p[q2.n++] = p->hdet + (size_t)j * L;
+          if (Utj) q2.p[q2.n++] = hqp(k0 + b, j, 1);
           if (T3j) {
             if (mag)
               add_adj(q2, k0 + b, j, 1);
@@ -260,15 +295,24 @@ struct Run {
           }
         }
         pbeg(p);
-        k_y2<L><<<L / G, NT, SM::XPT, p->stream>>>(p->V1, p->Aw, qjj, Gj, T3j, (size_t)nz * LL, tb, q2, mag, N, nb);
-        // bytes: V1 read, Aw read (G_j), T3 write per frame; G_j read + write and q_j once per batch
-        pend(p, HOLO_PASS_Y2, nb * (rN * A + (Gj ? A : 0) + (T3j ? A : 0)) + (Gj ? 2 * A : 0) + (T3j ? A : 0),
-             nb * L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0)));
+        if (ps)
+          k_y2<L, true><<<L / G, NT, SM::XPT, p->stream>>>(p->V1, p->Aw, nullptr, p->Qk, nullptr, Utj, T3j,
+                                                            (size_t)nz * LL, tb, q2, mag, N, nb);
+        else
+          k_y2<L, false><<<L / G, NT, SM::XPT, p->stream>>>(p->V1, p->Aw, qjj, nullptr, Gj, nullptr, T3j,
+                                                             (size_t)nz * LL, tb, q2, mag, N, nb);
+        // bytes: V1 read, Aw read (q gradient), T3 write per frame; G_j read + write and q_j once per batch
+        // (PS: Qk read per frame, Ut write per frame)
+        pend(p, HOLO_PASS_Y2,
+             nb * (rN * A + (want_q ? A : 0) + (T3j ? A : 0) + (ps ? ((T3j ? A : 0) + (want_q ? A : 0)) : 0)) +
+                 (Gj ? 2 * A : 0) + ((T3j && !ps) ? A : 0),
+             nb * L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0) + (Utj ? 1 : 0)));
       }
-      // ---- X3 (per angle): g_k = 2 IFFT_x( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3[b][j]
-      if (gpsi && (mode == 0 || mode == 2)) {
-        for (int b = 0; b < nb; b++) {
-          const int k = k0 + b;
+      // ---- X3 (per angle): g_k = 2 IFFT_x( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3[b][j];
+      //      PS: XG, Ghat (+)= sum_j conj(Hq_x) FFT_x(Ut[b][j])
+      for (int b = 0; b < nb; b++) {
+        const int k = k0 + b;
+        if (gpsi && (mode == 0 || mode == 2)) {
           TabSeq q3{};
           for (int j = 0; j < nz; j++) {
             if ((p->magmask >> j) & 1u)
@@ -282,9 +326,28 @@ struct Run {
                                                       q3, nz, p->magmask, gscale);
           pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
         }
+        if (ps && gq_pass) {
+          TabSeq qg{};
+          for (int j = 0; j < nz; j++) qg.p[qg.n++] = hqp(k, j, 0);
+          pbeg(p);
+          k_xg<L><<<L / G, NT, SM::XPT, p->stream>>>(p->Ut + (size_t)b * nz * LL, p->Ghat, tb, qg, nz, k == 0);
+          pend(p, HOLO_PASS_PS, (nz + (k ? 2 : 1)) * A, L * fl * nz);
+        }
       }
     }
-    if (want_q && (mode == 0 || mode == 2)) gq(p, gq_out, gscale, acc_q);
+    // reference frames of the fused objective (O14 into the same Ghat / F)
+    if (sqrt_dref && p->n_ref > 0 && mode == 0) {
+      if (!ps) RefRun<L>::qhat(p, q);
+      RefRun<L>::frames(p, sqrt_dref, want_q, /*first=*/!ps);
+    }
+    if (gq_pass) {
+      if (ps) {
+        RefRun<L>::final(p, gq_out, gscale, acc_q);
+      } else {
+        gq(p, gq_out, gscale, acc_q);
+        if (sqrt_dref && p->n_ref > 0 && mode == 0) RefRun<L>::final(p, gq_out, gscale, true);
+      }
+    }
   }
 };
 
@@ -340,18 +403,26 @@ struct RefRun {
     pend(p, HOLO_PASS_REF, 6 * A, 2.0 * L * fl, 3);
   }
 
-  static void run(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc) {
+  // Qhat = DFT2(q)  (P2 [fy][fx])
+  static void qhat(holo_plan *p, const float2 *q) {
+    const int N = p->N;
+    const size_t SM = E::SMEM;
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const int gl = L / E::G;
+    pbeg(p);
+    k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, p->tw3, N, 1.f, 0);
+    k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, p->tw3, N, 0);
+    pend(p, HOLO_PASS_REF, 4 * 8.0 * L * L, 2.0 * L * fftf(L), 2);
+  }
+
+  // the R reference frames: F partials -> partR; with want_q, Ghat (+)= conj(H) DFT2(Z rho^r)
+  static void frames(holo_plan *p, const float *sqrt_dref, bool want_q, bool first) {
     const int N = p->N, R = p->n_ref;
     const size_t SM = E::SMEM;
     const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
     const float2 *tw3 = p->tw3;
     const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
     const double A = 8.0 * L * L, fl = fftf(L);
-    // Qhat = DFT2(q)
-    pbeg(p);
-    k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, tw3, N, 1.f, 0);
-    k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, tw3, N, 0);
-    pend(p, HOLO_PASS_REF, 4 * A, 2.0 * L * fl, 2);
     for (int r = 0; r < R; r++) {
       const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
       pbeg(p);
@@ -359,20 +430,40 @@ struct RefRun {
       k_ref_rows<L, REF_R2><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r * N * N, p->Vr,
                                                             p->partR + (size_t)r * gn, Hx, tw, tw3, N, 1.f, 0,
                                                             p->tau2);
-      if (gq) k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, tw3, N, r == 0);
-      pend(p, HOLO_PASS_REF, A * (1.0 + 0.5 + 0.5 + 1.0 / 8 + 0.5 + (gq ? 0.5 + (r ? 2.0 : 1.0) : 0.0)),
-           fl * (L + 2.0 * N + (gq ? L : 0)), gq ? 3 : 2);
+      if (want_q) k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, tw3, N, first && r == 0);
+      pend(p, HOLO_PASS_REF,
+           A * (1.0 + 0.5 + 0.5 + 1.0 / 8 + 0.5 + (want_q ? 0.5 + ((first && r == 0) ? 1.0 : 2.0) : 0.0)),
+           fl * (L + 2.0 * N + (want_q ? L : 0)), want_q ? 3 : 2);
     }
-    if (gq) {
-      pbeg(p);
-      k_ref_cols<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, p->Ghat, nullptr, tw, tw3, N, 0);
-      k_ref_rows<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, nullptr, gq, nullptr, nullptr, tw, tw3, N,
-                                                               2.0f, acc ? 1 : 0);
-      pend(p, HOLO_PASS_REF, (acc ? 5 : 4) * A, 2.0 * L * fl, 2);
-    }
+  }
+
+  // gq (+)= scale * IDFT2(Ghat)
+  static void final(holo_plan *p, float2 *gq, float scale, bool acc) {
+    const int N = p->N;
+    const size_t SM = E::SMEM;
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const int gl = L / E::G;
+    const double A = 8.0 * L * L;
     pbeg(p);
-    k_reduce<<<1, 1024, 0, p->stream>>>(p->partR, (size_t)R * gn, 1, sc, 0);
-    pend(p, HOLO_PASS_REDUCE, 8.0 * R * gn, 0);
+    k_ref_cols<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, p->Ghat, nullptr, tw, p->tw3, N, 0);
+    k_ref_rows<L, REF_FINAL><<<gl, E::NT, SM, p->stream>>>(p->Ghat, nullptr, gq, nullptr, nullptr, tw, p->tw3, N,
+                                                             scale, acc ? 1 : 0);
+    pend(p, HOLO_PASS_REF, (acc ? 5 : 4) * A, 2.0 * L * fftf(L), 2);
+  }
+
+  // sc[0] (+)= sum of the reference frames' F partials
+  static void reduce(holo_plan *p, double *sc, bool acc) {
+    const int gn = (p->N + E::G - 1) / E::G;
+    pbeg(p);
+    k_reduce<<<1, 1024, 0, p->stream>>>(p->partR, (size_t)p->n_ref * gn, 1, sc, acc ? 1 : 0);
+    pend(p, HOLO_PASS_REDUCE, 8.0 * p->n_ref * gn, 0);
+  }
+
+  static void run(holo_plan *p, const float2 *q, const float *sqrt_dref, float2 *gq, double *sc, bool acc) {
+    qhat(p, q);
+    frames(p, sqrt_dref, gq != nullptr, true);
+    if (gq) final(p, gq, 2.0f, acc);
+    reduce(p, sc, false);
   }
 };
 

@@ -27,10 +27,12 @@ class JointCG:
     a plan with n_angles = 0 then runs the probe-only problem of configs[4] (rho_psi unused)."""
 
     def __init__(self, plan, sqrt_d, psi0, q0, rho_psi=1.0, rho_q=1.0, gamma_init=1.0, max_halvings=12,
-                 group=None, distributed=None, sqrt_dref=None):
+                 group=None, distributed=None, sqrt_dref=None, fused=None):
         self.plan = plan
         self.d = sqrt_d
         self.dref = sqrt_dref
+        # holo_grad_full when the plan provides it (the CPU test double of the dist tests does not)
+        self.fused = hasattr(plan, "grad_full") if fused is None else bool(fused)
         self.rho = (float(rho_psi), float(rho_q))
         self.gamma_init, self.max_halvings = float(gamma_init), int(max_halvings)
         self.group = group
@@ -58,10 +60,14 @@ class JointCG:
         """F and grad at (psi, q); returns host (F, gg_psi, geta_psi, gg_q, geta_q)."""
         p = self.plan
         sc3 = self.sc[:3]
-        # always called, also on a rank without angles: holo_grad then writes F = 0 and a ZERO
-        # probe-gradient partial, so no stale (already reduced) g_q enters the allreduce
-        p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
-        if self.dref is not None:  # reference arm: F_ref into sc[0], its gradient added to g_q
+        # always called, also on a rank without angles: the library then writes F = 0 and a ZERO
+        # probe-gradient partial, so no stale (already reduced) g_q enters the allreduce.
+        if self.dref is None:
+            p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
+        elif self.fused:  # the whole Eq. (10): object frames + reference frames in one sweep
+            p.grad_full(psi, q, self.d, self.dref, sc3, eta_psi, g_psi, g_q)
+        else:  # reference arm as a second call: F_ref into sc[0], its gradient added to g_q
+            p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
             p.grad_ref(q, self.dref, self.scr, g_q, flags=HOLO_ACCUMULATE_Q)
             sc3[:1] += self.scr
         if self.dist:
