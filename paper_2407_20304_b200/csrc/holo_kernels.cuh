@@ -79,6 +79,14 @@ struct Priv {
   __device__ __forceinline__ float2 &operator[](int r) const { return p[r * NT + threadIdx.x]; }
 };
 
+// Fire-and-forget accumulate (REDG.ADD.F32x2): for accumulators with ONE writer thread per
+// element (a column's owner across the batch, a row's owner across planes), so the result is the
+// same sequential sum as a read-modify-write, without the load round trip (fp32 RN; the L2 ALU
+// flushes denormals, irrelevant at |x| >> 1e-38).  A later read by the same thread uses __ldcg.
+__device__ __forceinline__ void red_add2(float2 *p, float2 v) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
 // ---- layout-S line I/O ----------------------------------------------------------
 template <int L>
 __device__ __forceinline__ void ld_row(float2 (&v)[16], const float2 *__restrict__ row, int t) {
@@ -135,48 +143,66 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                : "memory");
 }
 
+// Table slots: 2 (default; table i + 1 streams into the other slot while table i is in use)
+// or 1 (HOLO_TAB_SLOTS=1, for two CTAs per SM: the slot is refilled by done() right after
+// each use, so the load overlaps the transform that follows).
+#ifndef HOLO_TAB_SLOTS
+#define HOLO_TAB_SLOTS 2
+#endif
 template <int L>
 struct TabPipe {
-  float2 *slot;   // 2 * L float2 of shared memory
-  uint64_t *bar;  // 2 mbarriers in shared memory
+  static constexpr int SLOTS = HOLO_TAB_SLOTS;
+  float2 *slot;   // SLOTS * L float2 of shared memory
+  uint64_t *bar;  // SLOTS mbarriers in shared memory
   int used;       // tables taken so far (uniform over the CTA)
-  static constexpr size_t BYTES = 2 * sizeof(float2) * L;
+  static constexpr size_t BYTES = SLOTS * sizeof(float2) * L;
 
   __device__ __forceinline__ void issue(const TabSeq &q, int i) {
     if (threadIdx.x == 0 && i < q.n) {
       fence_proxy_async();  // earlier generic reads of this slot precede the async write
-      mbar_expect_tx(bar + (i & 1), L * sizeof(float2));
-      bulk_g2s(slot + (i & 1) * L, q.p[i], L * sizeof(float2), bar + (i & 1));
+      mbar_expect_tx(bar + (i & (SLOTS - 1)), L * sizeof(float2));
+      bulk_g2s(slot + (i & (SLOTS - 1)) * L, q.p[i], L * sizeof(float2), bar + (i & (SLOTS - 1)));
     }
   }
-  // all threads; starts tables 0 and 1
+  // all threads; starts the first table(s)
   __device__ __forceinline__ void start(const TabSeq &q, float2 *sm_slots, uint64_t *bars) {
     slot = sm_slots;
     bar = bars;
     used = 0;
     if (threadIdx.x == 0) {
-      mbar_init(bar, 1);
-      mbar_init(bar + 1, 1);
+      for (int b = 0; b < SLOTS; b++) mbar_init(bar + b, 1);
       fence_mbar_init();
     }
     __syncthreads();
-    issue(q, 0);
-    issue(q, 1);
+    for (int b = 0; b < SLOTS; b++) issue(q, b);
   }
-  // Table i = used: wait for it, then refill the other slot with table i + 1 (its
-  // previous content, table i - 1, was consumed before a transform barrier; pass
-  // sync = true when no transform separates the use of table i - 1 from this call).
+  // Table i = used.  Two slots: wait for it, then refill the other slot with table i + 1 (its
+  // previous content, table i - 1, was consumed before a transform barrier; pass sync = true
+  // when no transform separates the use of table i - 1 from this call).  One slot: just wait
+  // (done() refilled it).
   __device__ __forceinline__ const float2 *take(const TabSeq &q, bool sync = false) {
     const int i = used++;
-    if (i >= 1) {
-      // the slot being refilled held table i - 1: every LINE must be done with it.  The
-      // transforms' barriers guarantee that only within a line when lines sync
-      // independently (HOLO_TMAJOR), so then the CTA syncs here.
-      if (sync || HOLO_TMAJOR) __syncthreads();
-      issue(q, i + 1);
+    if constexpr (SLOTS == 2) {
+      if (i >= 1) {
+        // the slot being refilled held table i - 1: every LINE must be done with it.  The
+        // transforms' barriers guarantee that only within a line when lines sync
+        // independently (HOLO_TMAJOR), so then the CTA syncs here.
+        if (sync || HOLO_TMAJOR) __syncthreads();
+        issue(q, i + 1);
+      }
+      mbar_wait(bar + (i & 1), (i >> 1) & 1);
+      return slot + (i & 1) * L;
+    } else {
+      mbar_wait(bar, i & 1);
+      return slot;
     }
-    mbar_wait(bar + (i & 1), (i >> 1) & 1);
-    return slot + (i & 1) * L;
+  }
+  // after the last read of the table just taken (all threads): one slot -> refill it now
+  __device__ __forceinline__ void done(const TabSeq &q) {
+    if constexpr (SLOTS == 1) {
+      __syncthreads();
+      issue(q, used);
+    }
   }
 };
 
@@ -218,10 +244,12 @@ __device__ __forceinline__ void mag_fwd(float2 (&v)[16], Src src, Stash stash, U
   const float2 *tab = pipe.take(q, sync0);  // cr
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r ^ 8] = cmul(src(r), tab[t + r * T]);
+  pipe.done(q);
   fft<L, false>(v, x, t, tw);
   tab = pipe.take(q);  // bke
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmul(v[r], tab[t + r * T]);
+  pipe.done(q);
   fft<L, true>(v, x, t, tw);
   tab = pipe.take(q);  // cr again
   const float2 wb = wodd_base(t, L);
@@ -235,16 +263,19 @@ __device__ __forceinline__ void mag_fwd(float2 (&v)[16], Src src, Stash stash, U
   HOLO_B(0) HOLO_B(1) HOLO_B(2) HOLO_B(3) HOLO_B(4) HOLO_B(5) HOLO_B(6) HOLO_B(7)
   HOLO_B(8) HOLO_B(9) HOLO_B(10) HOLO_B(11) HOLO_B(12) HOLO_B(13) HOLO_B(14) HOLO_B(15)
 #undef HOLO_B
+  pipe.done(q);
   fft<L, false>(v, x, t, tw);
   tab = pipe.take(q);  // bko
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmul(v[r], tab[t + r * T]);
+  pipe.done(q);
   fft<L, true>(v, x, t, tw);
   tab = pipe.take(q);  // cout
 #define HOLO_C(R) v[R] = cmul(cadd(unstash(R), cmulc(v[R], wodd_q<R>(wb))), tab[t + (R) * T]);
   HOLO_C(0) HOLO_C(1) HOLO_C(2) HOLO_C(3) HOLO_C(4) HOLO_C(5) HOLO_C(6) HOLO_C(7)
   HOLO_C(8) HOLO_C(9) HOLO_C(10) HOLO_C(11) HOLO_C(12) HOLO_C(13) HOLO_C(14) HOLO_C(15)
 #undef HOLO_C
+  pipe.done(q);
 }
 
 // Adjoint (M S)^* along the line (the steps of mag_fwd conjugated, in reverse):
@@ -260,10 +291,12 @@ __device__ __forceinline__ void mag_adj(float2 (&v)[16], Src src, Stash stash, U
   const float2 *tab = pipe.take(q, sync0);  // cout
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(src(r), tab[t + r * T]);
+  pipe.done(q);
   fft<L, false>(v, x, t, tw);
   tab = pipe.take(q);  // bke
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], tab[t + r * T]);
+  pipe.done(q);
   fft<L, true>(v, x, t, tw);
   tab = pipe.take(q);  // cout again
   const float2 wb = wodd_base(t, L);
@@ -277,10 +310,12 @@ __device__ __forceinline__ void mag_adj(float2 (&v)[16], Src src, Stash stash, U
   HOLO_B(0) HOLO_B(1) HOLO_B(2) HOLO_B(3) HOLO_B(4) HOLO_B(5) HOLO_B(6) HOLO_B(7)
   HOLO_B(8) HOLO_B(9) HOLO_B(10) HOLO_B(11) HOLO_B(12) HOLO_B(13) HOLO_B(14) HOLO_B(15)
 #undef HOLO_B
+  pipe.done(q);
   fft<L, false>(v, x, t, tw);
   tab = pipe.take(q);  // bko
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], tab[t + r * T]);
+  pipe.done(q);
   fft<L, true>(v, x, t, tw);
 #define HOLO_Z(R) s[R] = cadd(unstash(R), cmulc(v[R], wodd_q<R>(wb)));
   HOLO_Z(0) HOLO_Z(1) HOLO_Z(2) HOLO_Z(3) HOLO_Z(4) HOLO_Z(5) HOLO_Z(6) HOLO_Z(7)
@@ -289,6 +324,7 @@ __device__ __forceinline__ void mag_adj(float2 (&v)[16], Src src, Stash stash, U
   tab = pipe.take(q);  // cr
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(s[r ^ 8], tab[t + r * T]);
+  pipe.done(q);
 }
 
 // ---- deterministic block reduction --------------------------------------------------

@@ -19,7 +19,7 @@ namespace holo {
 
 // coarse rows (row-major [L2/2][L2/2]) -> P2 scratch [L2/2 rows][L2]
 template <int L2>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_up_rows(const float2 *__restrict__ in, float2 *__restrict__ mid, const float4 *__restrict__ tw,
               const float2 *__restrict__ up) {
   using C = CtaK<L2>;
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 // columns of the P2 scratch (L2/2 rows) -> fine row-major [L2][L2]
 template <int L2>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_up_cols(const float2 *__restrict__ mid, float2 *__restrict__ out, const float4 *__restrict__ tw,
               const float2 *__restrict__ up) {
   using C = CtaK<L2>;

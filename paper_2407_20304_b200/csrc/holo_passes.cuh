@@ -11,7 +11,14 @@
 
 namespace holo {
 
-constexpr int NT = 512;
+// Threads per CTA of the object-chain line kernels (HOLO_NT): 512 = G = 8192/L lines per CTA and one
+// CTA per SM at <= 128 registers; 256 = half the lines and two CTAs per SM (their shared-memory
+// and FP32 phases can overlap; needs HOLO_TAB_SLOTS=1 to fit two CTAs' shared memory at L = 4096).
+#ifndef HOLO_NT
+#define HOLO_NT 512
+#endif
+constexpr int NT = HOLO_NT;
+constexpr int CTAS_PER_SM = 512 / NT;
 template <int L>
 using CtaK = Cta<L, NT>;
 
@@ -71,13 +78,14 @@ __device__ __noinline__ void x1_plane(float2 *__restrict__ T1j, const float4 *__
     const float2 *cr = pipe.take(seq, sync0);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(X[r], cr[t + r * (L / 16)]);
+    pipe.done(seq);
     fft<L, true>(v, x, t, tw);
   }
   st_p2_row<L>(v, T1j, y, L, t);
 }
 
 template <int L>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1, Tables tb, const __grid_constant__ TabSeq seq,
          int nz, uint32_t magmask) {
   using C = CtaK<L>;
@@ -135,6 +143,7 @@ __device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float
     const float2 *cr = pipe.take(seq);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], cr[t + r * T]);
+    pipe.done(seq);
     fft<L, true>(v, x, t, tw);
   }
   if (aout) st_p2_col<L>(v, aout, col, L, t);
@@ -145,6 +154,7 @@ __device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float
     const float2 *hq = pipe.take(seq);  // Hq_y(k, j) = h_omega r_{s^p_y} / L
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], hq[t + r * T]);
+    pipe.done(seq);
     fft<L, true>(v, x, t, tw);
     st_p2_col<L>(v, qk, col, L, t);
     if (w1) {
@@ -160,6 +170,7 @@ __device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float
     const float2 *h = pipe.take(seq);  // hdet_j / L
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], h[t + r * T]);
+    pipe.done(seq);
     fft<L, true>(v, x, t, tw);
     const int o = (L - N) / 2;
 #pragma unroll
@@ -171,7 +182,7 @@ __device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float
 }
 
 template <int L, bool PS>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_y1(const float2 *__restrict__ T1j, size_t fstride, const float2 *__restrict__ qj, const float2 *__restrict__ Qt,
          float2 *__restrict__ Qk, float2 *__restrict__ Aout, float2 *__restrict__ W1, Tables tb,
          const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
@@ -182,10 +193,11 @@ __global__ void __launch_bounds__(NT, 1)
   TabPipe<L> pipe;
   pipe.start(seq, slot_base<L, true>(sm), bars);
   const int col0 = blockIdx.x * C::G;
+  constexpr int PF_COLS = C::G < 2 ? 2 : C::G;  // whole P2 column pairs (16-byte aligned blocks)
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *in = T1j + (size_t)b * fstride;
-    if (threadIdx.x == 0 && b + 1 < nb) prefetch_l2(in + fstride + p2(0, col0, L), 8u * C::G * L);
+    if (threadIdx.x == 0 && b + 1 < nb) prefetch_l2(in + fstride + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
     y1_frame<L, PS>(in, qj, PS ? Qt + (size_t)b * fstride : nullptr, (PS && Qk) ? Qk + (size_t)b * L * L : nullptr,
                     Aout ? Aout + (size_t)b * L * L : nullptr, W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq, pipe,
                     sm, mag, N);
@@ -200,7 +212,7 @@ __global__ void __launch_bounds__(NT, 1)
 //   OBJ : W1 row -> D_x, crop, F only
 // Strides between the batch's frames: in / out (elements), sqrt_d (elements), partial (CTAs).
 template <int L, int MODE>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x2(const float2 *__restrict__ in, size_t in_stride, const float *__restrict__ sqrt_d, size_t d_stride,
          float2 *__restrict__ out, size_t out_stride, double *__restrict__ partial, int part_stride, Tables tb,
          const __grid_constant__ TabSeq seq, int N, int tau2) {
@@ -237,6 +249,7 @@ __global__ void __launch_bounds__(NT, 1)
     const float2 *h = pipe.take(seq);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], h[t + r * T]);
+    pipe.done(seq);
     fft<L, true>(v, x, t, tb.tw);
     if (MODE == X2_FWD) {
       if (act) {
@@ -284,6 +297,7 @@ __global__ void __launch_bounds__(NT, 1)
   const float2 *h = pipe.take(seq);
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], h[t + r * T]);
+  pipe.done(seq);
   fft<L, true>(v, x, t, tb.tw);
   if (act) st_p2_row<L>(v, out, y, N, t);
 }
@@ -319,6 +333,7 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
     const float2 *h = pipe.take(seq);  // hdet_j / L, conjugated
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], h[t + r * T]);
+    pipe.done(seq);
   }
   fft<L, true>(v, x, t, tw);
   if (PS && ut) {
@@ -331,6 +346,7 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
     const float2 *hq = pipe.take(seq);  // Hq_y(k, j), conjugated
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], hq[t + r * T]);
+    pipe.done(seq);
     st_p2_col<L>(v, ut, col, L, t);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = Y[r];
@@ -338,7 +354,7 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const size_t gi = p2(t + r * T, col, L);
-      Gj[gi] = cadd(Gj[gi], cmulc(v[r], ldg2(ab + gi)));
+      red_add2(Gj + gi, cmulc(v[r], ldg2(ab + gi)));  // G_j += conj(a) v (this thread owns gi)
     }
   }
   if (!t3) return;
@@ -355,13 +371,14 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
     const float2 *cr = pipe.take(seq);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
+    pipe.done(seq);
   }
   fft<L, true>(v, x, t, tw);
   st_p2_col<L>(v, t3, col, L, t);
 }
 
 template <int L, bool PS>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_y2(const float2 *__restrict__ V1, const float2 *__restrict__ a, const float2 *__restrict__ qj,
          const float2 *__restrict__ Qk, float2 *__restrict__ Gj, float2 *__restrict__ Ut, float2 *__restrict__ T3j,
          size_t fstride, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
@@ -372,14 +389,15 @@ __global__ void __launch_bounds__(NT, 1)
   TabPipe<L> pipe;
   pipe.start(seq, slot_base<L, true>(sm), bars);
   const int col0 = blockIdx.x * C::G;
+  constexpr int PF_COLS = C::G < 2 ? 2 : C::G;  // whole P2 column pairs (16-byte aligned blocks)
   const bool wq = PS ? Ut != nullptr : Gj != nullptr;
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *vin = V1 + (size_t)b * N * L;
     const float2 *ab = a + (size_t)b * L * L;
     if (threadIdx.x == 0 && b + 1 < nb) {
-      prefetch_l2(vin + (size_t)N * L + p2(0, col0, N), 8u * C::G * N);
-      if (wq) prefetch_l2(ab + (size_t)L * L + p2(0, col0, L), 8u * C::G * L);
+      prefetch_l2(vin + (size_t)N * L + p2(0, col0 & ~1, N), 8u * PF_COLS * N);
+      if (wq) prefetch_l2(ab + (size_t)L * L + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
     }
     y2_frame<L, PS>(vin, ab, PS ? Qk + (size_t)b * L * L : qj, Gj, (PS && Ut) ? Ut + (size_t)b * fstride : nullptr,
                     T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N);
@@ -402,32 +420,38 @@ __device__ __noinline__ void x3_plane(const float2 *__restrict__ T3j, float2 *__
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 v[16];
   if (mag) {
-    // source re-read from global (L2) for the second half; the first half is parked privately
+    // the source row is read ONCE into the thread-private slot; the first half's term is
+    // parked in registers (as in X1)
+#pragma unroll
+    for (int r = 0; r < 16; r++) Z[r] = ldg2(T3j + p2(y, t + r * T, L));
+    float2 e[16];
     mag_adj<L>(
-        v, [&](int r) { return ldg2(T3j + p2(y, t + r * T, L)); }, [&](int r, float2 e) { Z[r] = e; },
-        [&](int r) { return Z[r]; }, pipe, seq, j > 0, x, t, tw);
+        v, [&](int r) { return Z[r]; }, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe,
+        seq, j > 0, x, t, tw);
   } else {
     ld_p2_row<L>(v, T3j, y, L, t);
     fft<L, false>(v, x, t, tw);
     const float2 *cr = pipe.take(seq);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
+    pipe.done(seq);
   }
-  if (j > 0) {
-#pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = cadd(grow[t + r * T], v[r]);
-  }
-  if (last) {
-#pragma unroll
-    for (int r = 0; r < 16; r++) Z[r] = v[r];  // the summed spectrum, for the final transform
-  } else {
+  // sum over planes in the g row (one owner thread per element): store, then fire-and-forget
+  // adds, and the last plane reads the sum back (L2, __ldcg) into the private slot
+  if (j == 0 && !last) {
 #pragma unroll
     for (int r = 0; r < 16; r++) grow[t + r * T] = v[r];
+  } else if (!last) {
+#pragma unroll
+    for (int r = 0; r < 16; r++) red_add2(grow + t + r * T, v[r]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; r++) Z[r] = j > 0 ? cadd(__ldcg(grow + t + r * T), v[r]) : v[r];
   }
 }
 
 template <int L>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x3(const float2 *__restrict__ T3, const float2 *__restrict__ eta, float2 *__restrict__ g,
          double *__restrict__ partial, Tables tb, const __grid_constant__ TabSeq seq, int nz, uint32_t magmask,
          float scale) {
@@ -474,7 +498,7 @@ __global__ void __launch_bounds__(NT, 1)
 // per axis, q_kj = IDFT_y(Hq_y IDFT_x(Hq_x Qhat)).
 // XQ (rows fy, one angle): Qt_j row = IFFT_x(Hq_x(k, j) Qhat row) for every plane j   (P2 [fy][x])
 template <int L>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_xq(const float2 *__restrict__ Qhat, float2 *__restrict__ Qt, Tables tb, const __grid_constant__ TabSeq seq,
          int nz) {
   using C = CtaK<L>;
@@ -499,6 +523,7 @@ __global__ void __launch_bounds__(NT, 1)
     const float2 *hq = pipe.take(seq, j > 0);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(X[r], hq[t + r * T]);
+    pipe.done(seq);
     fft<L, true>(v, x, t, tb.tw);
     st_p2_row<L>(v, Qt + (size_t)j * L * L, y, L, t);
   }
@@ -506,7 +531,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 // XG (rows fy, one angle): Ghat row (+)= sum_j conj(Hq_x(k, j)) FFT_x(Ut_j row)   (first: overwrite)
 template <int L>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_xg(const float2 *__restrict__ Ut, float2 *__restrict__ Ghat, Tables tb, const __grid_constant__ TabSeq seq,
          int nz, int first) {
   using C = CtaK<L>;
@@ -530,6 +555,7 @@ __global__ void __launch_bounds__(NT, 1)
       const float2 a = cmulc(v[r], hq[t + r * T]);
       S[r] = j == 0 ? a : cadd(S[r], a);
     }
+    pipe.done(seq);
   }
 #pragma unroll
   for (int r = 0; r < 16; r++) {
@@ -542,7 +568,7 @@ __global__ void __launch_bounds__(NT, 1)
 // rows: out = scale/L * IFFT(h^(*) FFT(in)) along x.
 // IN_P2 / OUT_P2: layout of in / out (else row-major); ACC: out += ...
 template <int L, bool IN_P2, bool OUT_P2, bool ACC>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_rows_filter(const float2 *__restrict__ in, float2 *__restrict__ out, Tables tb, const float2 *__restrict__ h,
                   int conj, float scale) {
   using C = CtaK<L>;
@@ -574,7 +600,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 // columns of a P2 array, in place allowed: out = scale/L * IFFT(h^(*) FFT(in)) along y
 template <int L>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_cols_filter(const float2 *__restrict__ in, float2 *__restrict__ out, Tables tb, const float2 *__restrict__ h,
                   int conj, float scale) {
   using C = CtaK<L>;

@@ -251,7 +251,7 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   holo_status s = HOLO_OK;
   const size_t LL = (size_t)L * L;
   auto A = [&](auto **ptr, size_t bytes) { if (s == HOLO_OK) s = dalloc(p, ptr, bytes); };
-  const int GR = 16 * 512 / L;  // lines per CTA of the object-chain line kernels (CtaK<L>::G, 512 threads)
+  const int GR = 16 * NT / L;  // lines per CTA of the object-chain line kernels (CtaK<L>::G)
   p->nbx2 = (N + GR - 1) / GR;
   p->nbx3 = L / GR;
   const size_t Kc = (size_t)(K > 0 ? K : 1);
