@@ -46,6 +46,7 @@ struct holo_plan {
   float2 *Qhat = nullptr, *Ghat = nullptr, *Wr = nullptr, *Vr = nullptr, *Href = nullptr, *tw3 = nullptr;
   double *partR = nullptr;
   int ref_cap = 0;  // frames Href / partR are sized for
+  int BR = 1;       // reference frames per batched launch (Wr / Vr hold BR frames)
   // multiresolution schedule (holo_multires.cuh): up-sampling table [L] and row-pass scratch P2 [L/2][L]
   float2 *uptab = nullptr, *Up = nullptr;
   // initial object (O18, holo_init.cuh): inverse-magnification Bluestein tables [nz][L] (mt' = 1/mt_j)

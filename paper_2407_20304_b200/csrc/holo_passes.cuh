@@ -61,8 +61,8 @@ __device__ __forceinline__ void st_p2_col(const float2 (&v)[16], float2 *__restr
 // (one non-inlined call per plane: only pointers and the pipe state cross it, so the
 // magnification keeps the whole register budget)
 template <int L>
-__device__ __noinline__ void x1_plane(float2 *__restrict__ T1j, const float4 *__restrict__ tw, const TabSeq &seq,
-                                      TabPipe<L> &pipe, float2 *sm, bool mag, bool sync0) {
+__device__ __noinline__ TabPipe<L> x1_plane(float2 *__restrict__ T1j, const float4 *__restrict__ tw, const TabSeq &seq,
+                                      TabPipe<L> pipe, float2 *sm, bool mag, bool sync0) {
   using C = CtaK<L>;
   Xch x = C::xch(sm);
   const Priv<NT> X{priv_base<L>(sm)};
@@ -82,6 +82,7 @@ __device__ __noinline__ void x1_plane(float2 *__restrict__ T1j, const float4 *__
     fft<L, true>(v, x, t, tw);
   }
   st_p2_row<L>(v, T1j, y, L, t);
+  return pipe;
 }
 
 template <int L>
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     for (int r = 0; r < 16; r++) X[r] = v[r];
   }
 #pragma unroll 1
-  for (int j = 0; j < nz; j++) x1_plane<L>(T1 + (size_t)j * L * L, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j > 0);
+  for (int j = 0; j < nz; j++) pipe = x1_plane<L>(T1 + (size_t)j * L * L, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j > 0);
 }
 
 // ----------------------------------------------------------------------------- Y1
@@ -121,10 +122,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // per-plane constant; its column comes from qt = IDFT_x(Hq_x Qhat) (XQ pass, spectral in y):
 // x Hq_y (table), IFFT_y -> q_kj column, stored to qk (Y2 needs conj(q_kj)).
 template <int L, bool PS>
-__device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float2 *__restrict__ qj,
+__device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const float2 *__restrict__ qj,
                                       const float2 *__restrict__ qt, float2 *__restrict__ qk,
                                       float2 *__restrict__ aout, float2 *__restrict__ w1, const float4 *__restrict__ tw,
-                                      const TabSeq &seq, TabPipe<L> &pipe, float2 *sm, int mag, int N) {
+                                      const TabSeq &seq, TabPipe<L> pipe, float2 *sm, int mag, int N) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   Xch x = C::xch(sm);
@@ -179,6 +180,7 @@ __device__ __noinline__ void y1_frame(const float2 *__restrict__ in, const float
       if (row >= 0 && row < N) w1[p2(row, col, N)] = v[r];
     }
   }
+  return pipe;
 }
 
 template <int L, bool PS>
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   for (int b = 0; b < nb; b++) {
     const float2 *in = T1j + (size_t)b * fstride;
     if (threadIdx.x == 0 && b + 1 < nb) prefetch_l2(in + fstride + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
-    y1_frame<L, PS>(in, qj, PS ? Qt + (size_t)b * fstride : nullptr, (PS && Qk) ? Qk + (size_t)b * L * L : nullptr,
+    pipe = y1_frame<L, PS>(in, qj, PS ? Qt + (size_t)b * fstride : nullptr, (PS && Qk) ? Qk + (size_t)b * L * L : nullptr,
                     Aout ? Aout + (size_t)b * L * L : nullptr, W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq, pipe,
                     sm, mag, N);
   }
@@ -312,10 +314,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // the y-spectrum with conj(Hq_y) and stored to ut (XG finishes the x axis and accumulates
 // the Fourier-domain sum, Eq. (12) with Q_kj^* = S_{-s^p} P_{-omega}); conj(q_kj) comes from qk.
 template <int L, bool PS>
-__device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const float2 *__restrict__ ab,
+__device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, const float2 *__restrict__ ab,
                                       const float2 *__restrict__ qj, float2 *__restrict__ Gj, float2 *__restrict__ ut,
                                       float2 *__restrict__ t3, const float4 *__restrict__ tw, const TabSeq &seq,
-                                      TabPipe<L> &pipe, float2 *sm, int mag, int N) {
+                                      TabPipe<L> pipe, float2 *sm, int mag, int N) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   Xch x = C::xch(sm);
@@ -357,7 +359,7 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
       red_add2(Gj + gi, cmulc(v[r], ldg2(ab + gi)));  // G_j += conj(a) v (this thread owns gi)
     }
   }
-  if (!t3) return;
+  if (!t3) return pipe;
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));  // qj: q_j, or q_kj (PS)
   if (mag) {
@@ -375,6 +377,7 @@ __device__ __noinline__ void y2_frame(const float2 *__restrict__ vin, const floa
   }
   fft<L, true>(v, x, t, tw);
   st_p2_col<L>(v, t3, col, L, t);
+  return pipe;
 }
 
 template <int L, bool PS>
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       prefetch_l2(vin + (size_t)N * L + p2(0, col0 & ~1, N), 8u * PF_COLS * N);
       if (wq) prefetch_l2(ab + (size_t)L * L + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
     }
-    y2_frame<L, PS>(vin, ab, PS ? Qk + (size_t)b * L * L : qj, Gj, (PS && Ut) ? Ut + (size_t)b * fstride : nullptr,
+    pipe = y2_frame<L, PS>(vin, ab, PS ? Qk + (size_t)b * L * L : qj, Gj, (PS && Ut) ? Ut + (size_t)b * fstride : nullptr,
                     T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N);
   }
 }
@@ -410,8 +413,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // The sum over planes is kept in the g row itself (L2-resident between planes); each plane
 // is one non-inlined call (spill-free magnification).
 template <int L>
-__device__ __noinline__ void x3_plane(const float2 *__restrict__ T3j, float2 *__restrict__ grow,
-                                      const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> &pipe, float2 *sm,
+__device__ __noinline__ TabPipe<L> x3_plane(const float2 *__restrict__ T3j, float2 *__restrict__ grow,
+                                      const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> pipe, float2 *sm,
                                       bool mag, int j, bool last) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
@@ -448,6 +451,7 @@ __device__ __noinline__ void x3_plane(const float2 *__restrict__ T3j, float2 *__
 #pragma unroll
     for (int r = 0; r < 16; r++) Z[r] = j > 0 ? cadd(__ldcg(grow + t + r * T), v[r]) : v[r];
   }
+  return pipe;
 }
 
 template <int L>
@@ -467,7 +471,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   float2 *grow = g + (size_t)y * L;  // also the Fourier-domain accumulator of sum_j W_j
 #pragma unroll 1
   for (int j = 0; j < nz; j++)
-    x3_plane<L>(T3 + (size_t)j * L * L, grow, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j, j + 1 == nz);
+    pipe = x3_plane<L>(T3 + (size_t)j * L * L, grow, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j, j + 1 == nz);
   Xch x = C::xch(sm);
   const Priv<NT> Z{priv_base<L>(sm)};
   float2 v[16];

@@ -417,6 +417,18 @@ holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
   // workspace of the reference arm, allocated on first use (shared with the probe-shift path)
   st = ensure_fourier_ws(p);
   if (st != HOLO_OK) return st;
+  {  // frame workspace of the batched reference passes: W_r, V_r [BR][N][L]
+    const int BR = n_ref < 8 ? (n_ref > 0 ? n_ref : 1) : 8;
+    if (!p->Wr || BR > p->BR) {
+      HC(cudaStreamSynchronize(p->stream));
+      dfree(p, (void **)&p->Wr);
+      dfree(p, (void **)&p->Vr);
+      st = dalloc(p, &p->Wr, sizeof(float2) * (size_t)N * L * BR);
+      if (st == HOLO_OK) st = dalloc(p, &p->Vr, sizeof(float2) * (size_t)N * L * BR);
+      if (st != HOLO_OK) return st;
+      p->BR = BR;
+    }
+  }
   if (n_ref > p->ref_cap) {  // (re)size the per-frame tables; the old ones are freed, not leaked
     const int G = p->ops->ref_lines_per_cta;
     const int nbr = (N + G - 1) / G;  // CTAs of one frame's R2 row pass (one F partial each)
@@ -516,8 +528,7 @@ holo_status ensure_fourier_ws(holo_plan *p) {
   const size_t LL = (size_t)p->L * p->L, NL = (size_t)p->N * p->L;
   holo_status st = dalloc(p, &p->Qhat, sizeof(float2) * LL);
   if (st == HOLO_OK) st = dalloc(p, &p->Ghat, sizeof(float2) * LL);
-  if (st == HOLO_OK) st = dalloc(p, &p->Wr, sizeof(float2) * NL);
-  if (st == HOLO_OK) st = dalloc(p, &p->Vr, sizeof(float2) * NL);
+  (void)NL;
   return st;
 }
 }  // namespace

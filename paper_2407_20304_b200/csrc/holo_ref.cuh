@@ -165,6 +165,72 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
   }
 }
 
+// ---------------------------------------------------------------- batched column passes
+// B_r reference frames per launch; frame b's tables at Href + 2 L b (x row, then y row).
+// R1B: the Qhat column is read ONCE; per frame: x Hy_b, inverse along y, rows [o, o+N) -> W_b
+template <int L>
+__global__ void __launch_bounds__(LineEng<L>::NT, 1)
+    k_ref_r1b(const float2 *__restrict__ Qhat, float2 *__restrict__ W, const float2 *__restrict__ Href, int nb,
+              const float4 *__restrict__ tw, const float2 *__restrict__ tw3, int N) {
+  using E = LineEng<L>;
+  extern __shared__ float4 sm4[];
+  typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
+  const int col = blockIdx.x * E::G + st.g;
+  const int o = (L - N) / 2;
+  float2 q0[16];
+#pragma unroll
+  for (int r = 0; r < 16; r++) q0[r] = ldg2(Qhat + p2(E::ifr(st, r), col, L));
+#pragma unroll 1
+  for (int b = 0; b < nb; b++) {
+    const float2 *Hy = Href + (size_t)b * 2 * L + L;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmul(q0[r], ldg2(Hy + E::ifr(st, r)));
+    E::inv(v, st, tw, tw3);
+    float2 *w = W + (size_t)b * N * L;
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int row = E::isp(st, r) - o;
+      if (row >= 0 && row < N) w[p2(row, col, N)] = v[r];
+    }
+  }
+}
+
+// R3B: per frame: pad(V_b col) -> forward along y -> x conj(Hy_b), summed over the batch in
+// registers; Ghat (+)= the sum: one read-modify-write of Ghat per batch instead of per frame
+template <int L>
+__global__ void __launch_bounds__(LineEng<L>::NT, 1)
+    k_ref_r3b(const float2 *__restrict__ V, float2 *__restrict__ Ghat, const float2 *__restrict__ Href, int nb,
+              const float4 *__restrict__ tw, const float2 *__restrict__ tw3, int N, int first) {
+  using E = LineEng<L>;
+  extern __shared__ float4 sm4[];
+  typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
+  const int col = blockIdx.x * E::G + st.g;
+  const int o = (L - N) / 2;
+  float2 acc[16];
+#pragma unroll
+  for (int r = 0; r < 16; r++) acc[r] = make_float2(0.f, 0.f);
+#pragma unroll 1
+  for (int b = 0; b < nb; b++) {
+    const float2 *vin = V + (size_t)b * N * L;
+    const float2 *Hy = Href + (size_t)b * 2 * L + L;
+    float2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int row = E::isp(st, r) - o;
+      v[r] = (row >= 0 && row < N) ? ldg2(vin + p2(row, col, N)) : make_float2(0.f, 0.f);
+    }
+    E::fwd(v, st, tw, tw3);
+#pragma unroll
+    for (int r = 0; r < 16; r++) acc[r] = cadd(acc[r], cmulc(v[r], ldg2(Hy + E::ifr(st, r))));
+  }
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    float2 *p = Ghat + p2(E::ifr(st, r), col, L);
+    *p = first ? acc[r] : cadd(*p, acc[r]);
+  }
+}
+
 // ---------------------------------------------------------------- row passes
 // QHAT : q row (row-major) -> forward along x -> Qx (P2)
 // R2   : W row (P2, N rows) x Hx -> inverse along x -> crop, residual (+F), pad ->
@@ -183,6 +249,14 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
   typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
   const int y = blockIdx.x * E::G + st.g;
   const int o = (L - N) / 2;
+  if (MODE == REF_R2 || MODE == REF_FWD || MODE == REF_INIT) {  // frame blockIdx.y of a batch
+    const size_t fb = blockIdx.y;
+    if (in) in += fb * N * L;
+    sqrt_d += fb * N * N;
+    out += fb * (MODE == REF_FWD ? (size_t)N * N : (size_t)N * L);
+    if (partial) partial += MODE == REF_INIT ? fb : fb * gridDim.x;
+    Hx += fb * 2 * L;
+  }
   float2 v[16];
   if (MODE == REF_QHAT) {
 #pragma unroll

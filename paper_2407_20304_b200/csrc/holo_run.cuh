@@ -62,6 +62,8 @@ void set_ref_attrs() {
   a((const void *)k_ref_rows<L, REF_FINAL>);
   a((const void *)k_ref_rows<L, REF_FWD>);
   a((const void *)k_ref_rows<L, REF_INIT>);
+  a((const void *)k_ref_r1b<L>);
+  a((const void *)k_ref_r3b<L>);
 }
 
 template <int L>
@@ -366,13 +368,14 @@ struct RefRun {
     k_ref_rows<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(q, nullptr, p->Qhat, nullptr, nullptr, tw, p->tw3, N, 1.f, 0);
     k_ref_cols<L, REF_QHAT><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Qhat, nullptr, tw, p->tw3, N, 0);
     pend(p, HOLO_PASS_REF, 4 * A, 2.0 * L * fl, 2);
-    for (int r = 0; r < R; r++) {
-      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
+    for (int r0 = 0; r0 < R; r0 += p->BR) {
+      const int nb = R - r0 < p->BR ? R - r0 : p->BR;
+      const float2 *H = p->Href + (size_t)r0 * 2 * L;
       pbeg(p);
-      k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, p->tw3, N, 0);
-      k_ref_rows<L, REF_FWD><<<gn, E::NT, SM, p->stream>>>(p->Wr, nullptr, w + (size_t)r * N * N, nullptr, Hx, tw,
-                                                             p->tw3, N, 1.f, 0);
-      pend(p, HOLO_PASS_REF, A * 2.0 + 8.0 * N * N, fl * (L + N), 2);
+      k_ref_r1b<L><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, p->tw3, N);
+      k_ref_rows<L, REF_FWD><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, nullptr, w + (size_t)r0 * N * N, nullptr, H,
+                                                                       tw, p->tw3, N, 1.f, 0);
+      pend(p, HOLO_PASS_REF, A + nb * (A + 8.0 * N * N), nb * fl * (L + N), 2);
     }
   }
 
@@ -387,13 +390,14 @@ struct RefRun {
     pbeg(p);
     k_frame_stats<<<R, 256, 0, p->stream>>>(sqrt_dref, NN, p->partR, nullptr);
     pend(p, HOLO_PASS_REDUCE, 4.0 * NN * R, 0);
-    for (int r = 0; r < R; r++) {
-      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
+    for (int r0 = 0; r0 < R; r0 += p->BR) {
+      const int nb = R - r0 < p->BR ? R - r0 : p->BR;
+      const float2 *H = p->Href + (size_t)r0 * 2 * L;
       pbeg(p);
-      k_ref_rows<L, REF_INIT><<<gn, E::NT, SM, p->stream>>>(nullptr, sqrt_dref + r * NN, p->Vr, p->partR + r, Hx, tw,
-                                                              p->tw3, N, 1.f, 0);
-      k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, p->tw3, N, r == 0);
-      pend(p, HOLO_PASS_REF, A * (0.0625 + 0.5 + 0.5 + (r ? 2.0 : 1.0)), fl * (N + L), 2);
+      k_ref_rows<L, REF_INIT><<<dim3(gn, nb), E::NT, SM, p->stream>>>(nullptr, sqrt_dref + r0 * NN, p->Vr,
+                                                                        p->partR + r0, H, tw, p->tw3, N, 1.f, 0);
+      k_ref_r3b<L><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, p->tw3, N, r0 == 0);
+      pend(p, HOLO_PASS_REF, nb * A * (0.0625 + 0.5 + 0.5) + A * (r0 ? 2.0 : 1.0), nb * fl * (N + L), 2);
     }
     pbeg(p);
     k_fill_mean<<<1184, 256, 0, p->stream>>>(q0, (size_t)L * L, p->partR, R);
@@ -423,17 +427,21 @@ struct RefRun {
     const float2 *tw3 = p->tw3;
     const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
     const double A = 8.0 * L * L, fl = fftf(L);
-    for (int r = 0; r < R; r++) {
-      const float2 *Hx = p->Href + (size_t)r * 2 * L, *Hy = Hx + L;
+    // B_r frames per launch: the Qhat column read once (R1B), Ghat read-modify-written once (R3B)
+    for (int r0 = 0; r0 < R; r0 += p->BR) {
+      const int nb = R - r0 < p->BR ? R - r0 : p->BR;
+      const float2 *H = p->Href + (size_t)r0 * 2 * L;
+      const bool f0 = first && r0 == 0;
       pbeg(p);
-      k_ref_cols<L, REF_R1><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, Hy, tw, tw3, N, 0);
-      k_ref_rows<L, REF_R2><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r * N * N, p->Vr,
-                                                            p->partR + (size_t)r * gn, Hx, tw, tw3, N, 1.f, 0,
-                                                            p->tau2);
-      if (want_q) k_ref_cols<L, REF_R3><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, Hy, tw, tw3, N, first && r == 0);
+      k_ref_r1b<L><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, tw3, N);
+      k_ref_rows<L, REF_R2><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
+                                                                      p->partR + (size_t)r0 * gn, H, tw, tw3, N, 1.f,
+                                                                      0, p->tau2);
+      if (want_q) k_ref_r3b<L><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, tw3, N, f0);
+      // bytes: Qhat once, W write + read, sqrt_d, V write + read per frame, Ghat once per batch
       pend(p, HOLO_PASS_REF,
-           A * (1.0 + 0.5 + 0.5 + 1.0 / 8 + 0.5 + (want_q ? 0.5 + ((first && r == 0) ? 1.0 : 2.0) : 0.0)),
-           fl * (L + 2.0 * N + (want_q ? L : 0)), want_q ? 3 : 2);
+           A + nb * A * (0.5 + 0.5 + 1.0 / 8 + 0.5 + (want_q ? 0.5 : 0.0)) + (want_q ? A * (f0 ? 1.0 : 2.0) : 0.0),
+           nb * fl * (L + 2.0 * N + (want_q ? L : 0)), want_q ? 3 : 2);
     }
   }
 
