@@ -100,6 +100,13 @@ holo_status holo_set_shifts(holo_plan *p, const double *s /*[host]*/);
  * a NULL s switches the path off again (plain q_j).  Power-of-two npad, n_angles > 0. */
 holo_status holo_set_probe_shifts(holo_plan *p, const double *s /*[host] | NULL*/);
 
+/* Overlap hook: `event` (a cudaEvent_t created by the caller, or NULL to clear) is
+ * recorded on the plan's stream by holo_grad / holo_grad_full / holo_adj as soon as grad_q_part
+ * (adj_q) is complete -- before the last angle batch's object-gradient (X3) passes -- so the
+ * caller can allreduce the probe-gradient partial on another stream while those passes run.
+ * The plan does not own the event. */
+holo_status holo_set_gq_event(holo_plan *p, void *event);
+
 /* Reference-frame shifts s^r_r (Eq. (10) reference term P:115; reading C16):
  * [host] float64 [n_ref][2] = (sx, sy).  Sets R = n_ref for holo_grad_ref. */
 holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s /*[host]*/);

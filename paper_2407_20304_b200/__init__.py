@@ -97,6 +97,9 @@ _lib.holo_set_probe_shifts.restype = _S
 _lib.holo_grad_full.argtypes = [_P, _P, _P, _P, _P, _P, _P, _P, _P, ctypes.c_uint32]
 _lib.holo_grad_full.restype = _S
 
+_lib.holo_set_gq_event.argtypes = [_P, _P]
+_lib.holo_set_gq_event.restype = _S
+
 _lib.holo_profile_enable.argtypes = [_P, ctypes.c_int]
 _lib.holo_profile_enable.restype = _S
 _lib.holo_profile_read.argtypes = [_P, _P, _P, _P, _P, ctypes.c_int]
@@ -111,7 +114,7 @@ EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes"
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
             "holo_grad_ref", "holo_fwd_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
             "holo_profile_read", "holo_upsample2", "holo_bin2", "holo_init_probe", "holo_init_psi",
-            "holo_set_probe_shifts", "holo_grad_full"]
+            "holo_set_probe_shifts", "holo_grad_full", "holo_set_gq_event"]
 
 
 class HoloError(RuntimeError):
@@ -206,6 +209,17 @@ class Plan:
     def set_shifts(self, s):
         s = np.ascontiguousarray(s, dtype=np.float64).reshape(self.K, self.nz, 2)
         self._chk(_lib.holo_set_shifts(self._h, s.ctypes.data_as(_P)))
+
+    def set_gq_event(self, event):
+        """holo_set_gq_event: a torch.cuda.Event recorded when grad_q_part is complete (None clears).
+        The event is recorded once here so that its CUDA handle exists; keep a reference to it."""
+        if event is None:
+            self._chk(_lib.holo_set_gq_event(self._h, None))
+            self._gq_event = None
+            return
+        event.record(self.stream)
+        self._gq_event = event
+        self._chk(_lib.holo_set_gq_event(self._h, ctypes.c_void_p(event.cuda_event)))
 
     def set_probe_shifts(self, s):
         """holo_set_probe_shifts: per-frame probe shifts s^p [K][nz][2] (None: plain q_j path)."""

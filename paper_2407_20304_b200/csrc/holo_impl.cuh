@@ -55,6 +55,7 @@ struct holo_plan {
   // per-frame probe shifts (O19, holo_set_probe_shifts): Hq [K][nz][2][L] = h_omega_j r_{s^p_kj} / L per axis;
   // Qt [B][nz][L][L] (IDFT_x(Hq_x Qhat), P2), Qk [B][L][L] (q_kj, P2), Ut [B][nz][L][L] (probe-gradient terms)
   bool ps = false;
+  cudaEvent_t gq_event = nullptr;  // holo_set_gq_event: recorded when grad_q_part is complete
   float2 *hq = nullptr, *Qt = nullptr, *Qk = nullptr, *Ut = nullptr;
   // per-pass event profiling (holo_profile_*)
   struct Rec {

@@ -500,6 +500,7 @@ holo_status grad_impl(holo_plan *p, const void *psi, const void *q, const float 
     if (ref) {  // a reference-only shard: the reference arm alone
       p->ops->ref_run(p, (const float2 *)q, sqrt_dref, gq, sc, true);
     }
+    if (gq && p->gq_event) HC(cudaEventRecord(p->gq_event, p->stream));
     return postcheck(p);
   }
   p->ops->sweep(p, obj ? 3 : 0, (const float2 *)psi, (const float2 *)q, sqrt_d, nullptr, nullptr,
@@ -547,6 +548,13 @@ holo_status holo_grad_full(holo_plan *p, const void *psi, const void *q, const f
   holo_status st = precheck(p);
   if (st != HOLO_OK) return st;
   return grad_impl(p, psi, q, sqrt_d, sqrt_dref, eta_psi_prev, grad_psi, grad_q_part, sc, flags);
+}
+
+holo_status holo_set_gq_event(holo_plan *p, void *event) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  p->gq_event = reinterpret_cast<cudaEvent_t>(event);
+  return HOLO_OK;
 }
 
 holo_status holo_set_probe_shifts(holo_plan *p, const double *s) {

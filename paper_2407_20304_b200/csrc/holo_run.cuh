@@ -159,6 +159,27 @@ struct Run {
     }
   }
 
+  // the probe-gradient tail of a sweep: reference frames of the fused objective (O14 into the same
+  // Ghat / F), then g_q = 2 sum_j P_{-omega_j} G_j (or the final IDFT2 of Ghat); records gq_event
+  static void finish_q(holo_plan *p, const float2 *q, float2 *gq_out, float gscale, bool want_q, bool acc_q, int mode,
+                       const float *sqrt_dref) {
+    const bool ps = p->ps, gq_pass = want_q && (mode == 0 || mode == 2);
+    const bool ref = sqrt_dref && p->n_ref > 0 && mode == 0;
+    if (ref) {
+      if (!ps) RefRun<L>::qhat(p, q);
+      RefRun<L>::frames(p, sqrt_dref, want_q, /*first=*/!ps);
+    }
+    if (gq_pass) {
+      if (ps) {
+        RefRun<L>::final(p, gq_out, gscale, acc_q);
+      } else {
+        gq(p, gq_out, gscale, acc_q);
+        if (ref) RefRun<L>::final(p, gq_out, gscale, true);
+      }
+      if (p->gq_event) cudaEventRecord(p->gq_event, p->stream);
+    }
+  }
+
   // mode: 0 grad, 1 fwd, 2 adj (y given), 3 objective only.
   // With per-frame probe shifts (p->ps, O19) the probe enters through Qhat = DFT2 q (XQ -> Qt ->
   // q_kj in Y1) and the probe gradient is accumulated in the Fourier domain (Y2 -> Ut -> XG ->
@@ -311,45 +332,49 @@ struct Run {
              nb * L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0) + (Utj ? 1 : 0)));
       }
       // ---- X3 (per angle): g_k = 2 IFFT_x( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3[b][j];
-      //      PS: XG, Ghat (+)= sum_j conj(Hq_x) FFT_x(Ut[b][j])
-      for (int b = 0; b < nb; b++) {
+      //      PS: XG, Ghat (+)= sum_j conj(Hq_x) FFT_x(Ut[b][j]).
+      // In the LAST batch the probe gradient is completed first (XG, reference frames, g_q filters
+      // or the final IDFT2) and p->gq_event recorded, so a caller can allreduce g_q on another
+      // stream while this batch's X3 passes run (SURVEY 8e overlap).
+      const bool last_batch = k0 + nb >= K;
+      auto xg = [&](int b) {
         const int k = k0 + b;
-        if (gpsi && (mode == 0 || mode == 2)) {
-          TabSeq q3{};
-          for (int j = 0; j < nz; j++) {
-            if ((p->magmask >> j) & 1u)
-              add_adj(q3, k, j, 0);
-            else
-              q3.p[q3.n++] = crp(k, j, 0);
-          }
-          pbeg(p);
-          k_x3<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T3 + (size_t)b * nz * LL, eta ? eta + (size_t)k * LL : nullptr,
-                                                      gpsi + (size_t)k * LL, p->partX3 + (size_t)k * 2 * p->nbx3, tb,
-                                                      q3, nz, p->magmask, gscale);
-          pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
+        TabSeq qg{};
+        for (int j = 0; j < nz; j++) qg.p[qg.n++] = hqp(k, j, 0);
+        pbeg(p);
+        k_xg<L><<<L / G, NT, SM::XPT, p->stream>>>(p->Ut + (size_t)b * nz * LL, p->Ghat, tb, qg, nz, k == 0);
+        pend(p, HOLO_PASS_PS, (nz + (k ? 2 : 1)) * A, L * fl * nz);
+      };
+      auto x3 = [&](int b) {
+        const int k = k0 + b;
+        TabSeq q3{};
+        for (int j = 0; j < nz; j++) {
+          if ((p->magmask >> j) & 1u)
+            add_adj(q3, k, j, 0);
+          else
+            q3.p[q3.n++] = crp(k, j, 0);
         }
-        if (ps && gq_pass) {
-          TabSeq qg{};
-          for (int j = 0; j < nz; j++) qg.p[qg.n++] = hqp(k, j, 0);
-          pbeg(p);
-          k_xg<L><<<L / G, NT, SM::XPT, p->stream>>>(p->Ut + (size_t)b * nz * LL, p->Ghat, tb, qg, nz, k == 0);
-          pend(p, HOLO_PASS_PS, (nz + (k ? 2 : 1)) * A, L * fl * nz);
+        pbeg(p);
+        k_x3<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T3 + (size_t)b * nz * LL, eta ? eta + (size_t)k * LL : nullptr,
+                                                    gpsi + (size_t)k * LL, p->partX3 + (size_t)k * 2 * p->nbx3, tb, q3,
+                                                    nz, p->magmask, gscale);
+        pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
+      };
+      const bool want_x3 = gpsi && (mode == 0 || mode == 2);
+      if (!last_batch) {
+        for (int b = 0; b < nb; b++) {
+          if (want_x3) x3(b);
+          if (ps && gq_pass) xg(b);
         }
-      }
-    }
-    // reference frames of the fused objective (O14 into the same Ghat / F)
-    if (sqrt_dref && p->n_ref > 0 && mode == 0) {
-      if (!ps) RefRun<L>::qhat(p, q);
-      RefRun<L>::frames(p, sqrt_dref, want_q, /*first=*/!ps);
-    }
-    if (gq_pass) {
-      if (ps) {
-        RefRun<L>::final(p, gq_out, gscale, acc_q);
       } else {
-        gq(p, gq_out, gscale, acc_q);
-        if (sqrt_dref && p->n_ref > 0 && mode == 0) RefRun<L>::final(p, gq_out, gscale, true);
+        if (ps && gq_pass)
+          for (int b = 0; b < nb; b++) xg(b);
+        finish_q(p, q, gq_out, gscale, want_q, acc_q, mode, sqrt_dref);
+        if (want_x3)
+          for (int b = 0; b < nb; b++) x3(b);
       }
     }
+    if (K == 0) finish_q(p, q, gq_out, gscale, want_q, acc_q, mode, sqrt_dref);
   }
 };
 

@@ -27,7 +27,7 @@ class JointCG:
     a plan with n_angles = 0 then runs the probe-only problem of configs[4] (rho_psi unused)."""
 
     def __init__(self, plan, sqrt_d, psi0, q0, rho_psi=1.0, rho_q=1.0, gamma_init=1.0, max_halvings=12,
-                 group=None, distributed=None, sqrt_dref=None, fused=None):
+                 group=None, distributed=None, sqrt_dref=None, fused=None, overlap=True):
         self.plan = plan
         self.d = sqrt_d
         self.dref = sqrt_dref
@@ -45,6 +45,12 @@ class JointCG:
         self.g_psi, self.g_q = z(self.psi), z(self.q)
         self.gt_psi, self.gt_q = z(self.psi), z(self.q)
         self.sc = torch.zeros(5, dtype=torch.float64, device=dev)
+        # g_q / X3 overlap: only with CUDA tensors, an NCCL group and a plan exposing the hook
+        self.comm = self.gq_ev = None
+        if self.dist and dev.type == "cuda" and hasattr(plan, "set_gq_event") and overlap:
+            self.comm = torch.cuda.Stream(dev)
+            self.gq_ev = torch.cuda.Event()
+            plan.set_gq_event(self.gq_ev)
         self.scr = torch.zeros(1, dtype=torch.float64, device=dev)  # F of the reference arm
         self.F = None
         self.dots = None
@@ -71,9 +77,19 @@ class JointCG:
             p.grad_ref(q, self.dref, self.scr, g_q, flags=HOLO_ACCUMULATE_Q)
             sc3[:1] += self.scr
         if self.dist:
-            # exchange 1: probe-gradient partial (complex64 viewed as float32), exchange 2: scalars
-            dist.all_reduce(torch.view_as_real(g_q), group=self.group)
-            dist.all_reduce(sc3, group=self.group)
+            # exchange 1: probe-gradient partial (complex64 viewed as float32), exchange 2: scalars.
+            # With an overlap event (CUDA/NCCL), exchange 1 runs on a side stream that waits only for
+            # the event the library records as soon as g_q is complete, i.e. while the last angle
+            # batch's object-gradient passes still run on the plan's stream.
+            if self.comm is not None:
+                self.comm.wait_event(self.gq_ev)
+                with torch.cuda.stream(self.comm):
+                    dist.all_reduce(torch.view_as_real(g_q), group=self.group)
+                dist.all_reduce(sc3, group=self.group)
+                torch.cuda.current_stream(g_q.device).wait_stream(self.comm)
+            else:
+                dist.all_reduce(torch.view_as_real(g_q), group=self.group)
+                dist.all_reduce(sc3, group=self.group)
         p.q_dots(g_q, eta_q, self.sc[3:])
         s = self.sc.cpu().tolist()  # the single host sync of the sweep
         self.sweeps += 1

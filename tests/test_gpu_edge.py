@@ -125,3 +125,36 @@ def test_adjoint_identities_full_size():
     p.fwd(psi, x_q, w)                      # Q x: linear in q at fixed psi
     lhs, rhs = d(w, y), d(x_q, a_q)
     assert abs(lhs - rhs) / abs(lhs) < 1e-4
+
+
+def test_gq_event_marks_complete_probe_gradient():
+    """holo_set_gq_event (SURVEY 8e overlap): a side stream that waits ONLY on the event sees the
+    finished probe-gradient partial, although the last batch's X3 passes are still queued after it;
+    the event sits before X3 (it completes before the sweep's last kernel)."""
+    import paper_2407_20304_b200 as hb
+    cfg = synth.CONFIGS["cfg1"]
+    K = 12
+    rng = np.random.default_rng(21)
+    psi = np.exp(0.2j * rng.standard_normal((K, cfg.npad, cfg.npad)))
+    q = 1 + 0.2 * (rng.standard_normal((cfg.npad, cfg.npad)) + 1j * rng.standard_normal((cfg.npad, cfg.npad)))
+    d = 1 + 0.1 * rng.uniform(size=(K, cfg.nz, cfg.n, cfg.n))
+    p = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=0, angle_batch=4)
+    ev = torch.cuda.Event()
+    p.set_gq_event(ev)
+    side = torch.cuda.Stream()
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(K, cfg.npad, cfg.npad, dtype=torch.complex64, device="cuda")
+    gq = torch.zeros(cfg.npad, cfg.npad, dtype=torch.complex64, device="cuda")
+    snap = torch.empty_like(gq)
+    P, Q, D = dev(psi), dev(q), dev(d, torch.float32)
+    torch.cuda.synchronize()
+    p.grad(P, Q, D, sc, None, gpsi, gq)
+    side.wait_event(ev)
+    with torch.cuda.stream(side):
+        snap.copy_(gq)
+    done_at_event = torch.cuda.Event()
+    done_at_event.record(side)
+    torch.cuda.synchronize()
+    assert torch.equal(snap, gq)
+    assert float(gq.abs().max()) > 0
+    p.set_gq_event(None)
