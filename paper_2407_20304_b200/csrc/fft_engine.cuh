@@ -44,7 +44,14 @@
 
 namespace holo {
 
-__device__ __forceinline__ int P(int i) { return i + (i >> 4); }
+// Exchange padding.  HOLO_PAD2=1 (measured 3 % slower, off): P(i) = i + 2 (i / 16) keeps every 16-element run
+// 16-byte aligned, so a thread's contiguous first-stage run is written with STS.128 (half the
+// store instructions of the MIO-throttled exchange); reads stay one 128-byte wavefront per
+// 16 lanes.  HOLO_PAD2=0 (default): the round-1 padding i + i/16.
+#ifndef HOLO_PAD2
+#define HOLO_PAD2 0
+#endif
+__device__ __forceinline__ int P(int i) { return HOLO_PAD2 ? i + 2 * (i >> 4) : i + (i >> 4); }
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
@@ -257,7 +264,7 @@ struct Shape {
   static constexpr int F = L >> (4 * S16);   // first radix
   static constexpr int T = L / 16;           // threads per line
   static constexpr int PER = 16 / F;         // stage-0 butterflies per thread
-  static constexpr int LP = L + L / 16;      // padded line (float2)
+  static constexpr int LP = L + (HOLO_PAD2 ? 2 : 1) * (L / 16);  // padded line (float2)
   // twiddle rows (4 float2 = 2 float4 each): sum over radix-16 stages of Ns
   static constexpr int TWROWS = F * (pow16(S16) - 1) / 15;
   static_assert(F == 2 || F == 4 || F == 8 || F == 16, "unsupported L");
@@ -386,10 +393,31 @@ __device__ __forceinline__ void fft(float2 (&v)[16], Xch &x, const int t, const 
     for (int s = 0; s < F; s++) v[b + PER * s] = u[s];
   }
   float2 *buf = x.next<S::T>();
+#if HOLO_PAD2
+  // each run of F outputs is contiguous (and, for L >= 1024 where the line buffers' skew is even,
+  // 16-byte aligned) in the padded buffer: STS.128
+  if constexpr (L >= 1024) {
+#pragma unroll
+  for (int b = 0; b < PER; b++) {
+    float4 *dst = reinterpret_cast<float4 *>(buf + P((t + S::T * b) * F));
+#pragma unroll
+    for (int s = 0; s < F; s += 2) {
+      const float2 lo = v[b + PER * s], hi = v[b + PER * (s + 1)];
+      dst[s / 2] = make_float4(lo.x, lo.y, hi.x, hi.y);
+    }
+  }
+  } else {
+#pragma unroll
+    for (int b = 0; b < PER; b++)
+#pragma unroll
+      for (int s = 0; s < F; s++) buf[P((t + S::T * b) * F + s)] = v[b + PER * s];
+  }
+#else
 #pragma unroll
   for (int b = 0; b < PER; b++)
 #pragma unroll
     for (int s = 0; s < F; s++) buf[P((t + S::T * b) * F + s)] = v[b + PER * s];
+#endif
   x.sync<S::T>();
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = buf[P(t + r * S::T)];

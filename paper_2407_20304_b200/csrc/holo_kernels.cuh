@@ -52,7 +52,7 @@ struct Cta {
   static constexpr int LPB = (LP + 15) / 16 * 16;  // one buffer, 16-float2 aligned
   // per-group stride (two buffers) skewed so that the groups sharing a 16-lane
   // phase land on distinct banks
-  static constexpr int SKEW = G <= 16 ? 16 / G : 1;
+  static constexpr int SKEW = G <= 16 ? 16 / G : 1;  // 16 lines/warp-half pairs on distinct banks; even for G <= 8
   static constexpr int GS = (HOLO_SINGLE_BUF ? 1 : 2) * LPB + SKEW;
   static constexpr size_t XBYTES = sizeof(float2) * (size_t)GS * G;
   static constexpr size_t PRIV = sizeof(float2) * 16 * NT;  // one thread-private line
