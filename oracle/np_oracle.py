@@ -119,13 +119,16 @@ class Problem:
     def frame_grad(self, psi_k, qj, j, s, sqrt_d, tau=1):
         """One frame (k, j): returns F_kj, 2 L_kj^* rho, and conj(a) v (the G_j term, no 2, no P_{-omega}).
         tau = 1: F_1 (Eq. (10)), rho = w - sqrt_d w/|w|;  tau = 2: F_2 (Eq. (9)), F = (|w|^2 - d)^2,
-        rho = h'(|w|^2) w = 2 (|w|^2 - d) w  (App. A.3 proposition with h(t) = (t - d)^2)."""
+        rho = h'(|w|^2) w = 2 (|w|^2 - d) w  (App. A.3 proposition with h(t) = (t - d)^2); any other
+        tau: the general penalty G_tau (residual_tau)."""
         w, a = self.frame_fwd(psi_k, qj, j, s)
         m = np.abs(w)
         if tau == 2:
             dm = m ** 2 - sqrt_d ** 2
             F = float(np.sum(dm ** 2))
             rho = 2.0 * dm * w
+        elif tau != 1:  # general G_tau (App. A.3)
+            F, rho = residual_tau(w, np.asarray(sqrt_d, np.float64), tau)
         else:
             F = float(np.sum((m - sqrt_d) ** 2))
             with np.errstate(invalid="ignore", divide="ignore"):
@@ -212,12 +215,27 @@ def grad_ref(wavelength, p0, zeta0, q, ref_shifts, sqrt_dref, want_q=True, tau=1
             dm = m ** 2 - a ** 2
             F += float(np.sum(dm ** 2))
             rho = 2.0 * dm * w
+        elif tau != 1:  # general G_tau (App. A.3)
+            Fr, rho = residual_tau(w, a, tau)
+            F += Fr
         else:
             F += float(np.sum((m - a) ** 2))
             rho = np.where(m > 0, w - a * w / np.where(m > 0, m, 1.0), 0.0)
         if want_q:
             gq += 2.0 * shift(prop(zpad(rho, L), wavelength, p0, -zeta0), -sx, -sy)
     return F, gq
+
+
+def residual_tau(w, a, tau):
+    """G_tau penalty of App. A.3 for general tau > 0, written out from the proposition:
+    h(phi) = (phi^{tau/2} - a^tau)^2, phi = |w|^2  ->  F = sum h(|w|^2),
+    h'(phi) = tau (phi^{tau/2} - a^tau) phi^{tau/2 - 1}  ->  rho = h'(|w|^2) w  (0 where w = 0, reading C7).
+    The gradient is 2 L^*(rho) (the proposition's 2 L^*(H'(|L psi|^2) . L psi))."""
+    phi = np.abs(w) ** 2
+    with np.errstate(invalid="ignore", divide="ignore"):
+        dm = np.where(phi > 0, phi ** (tau / 2.0), 0.0) - a ** tau
+        hp = np.where(phi > 0, tau * dm * np.where(phi > 0, phi, 1.0) ** (tau / 2.0 - 1.0), 0.0)
+    return float(np.sum(dm ** 2)), hp * w
 
 
 def upsample2(x):

@@ -477,3 +477,67 @@ def test_f2_reference_arm_finite_differences():
     Fm = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q - h * v, rs, d, False, tau=2)[0]
     fd = (Fp - Fm) / (2 * h)
     assert abs(fd - np.vdot(gq, v).real) / abs(fd) < 1e-6
+
+
+@pytest.mark.parametrize("tau", [0.5, 1.5, 3.0])
+def test_g_tau_objective_finite_differences(tau):
+    """General penalty G_tau (App. A.3) in the numpy oracle: central finite differences
+    of G_tau in psi and q directions equal Re<v, 2 L^*(h'(|Lpsi|^2) Lpsi)> (the proposition), and
+    G_tau = 0, grad = 0 at exact data."""
+    cfg = synth.CONFIGS["cfg0"]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    L, N, K = 16, 8, 2
+    rng = np.random.default_rng(31)
+    psi = np.exp(1j * 0.3 * rng.standard_normal((K, L, L)))
+    q = 1 + 0.2 * (rng.standard_normal((L, L)) + 1j * rng.standard_normal((L, L)))
+    s = rng.uniform(-2, 2, size=(K, 2, 2))
+    pr = npo.Problem(g, L, N)
+    out = pr.fwd(psi, q, s)
+    d_exact = np.stack([np.stack([np.abs(out[(k, j)]) for j in range(2)]) for k in range(K)])
+    F0, gp0, gq0 = pr.grad(psi, q, s, d_exact, tau=tau)
+    assert F0 < 1e-20 and np.abs(gp0).max() < 1e-10 and np.abs(gq0).max() < 1e-10
+    d = d_exact * np.abs(1 + 0.3 * rng.standard_normal(d_exact.shape))
+    F, gp, gq = pr.grad(psi, q, s, d, tau=tau)
+    h = 1e-6
+    vp = rng.standard_normal(psi.shape) + 1j * rng.standard_normal(psi.shape)
+    fd = (pr.grad(psi + h * vp, q, s, d, tau=tau)[0] - pr.grad(psi - h * vp, q, s, d, tau=tau)[0]) / (2 * h)
+    assert abs(fd - np.vdot(gp, vp).real) / abs(fd) < 1e-6
+    vq = rng.standard_normal(q.shape) + 1j * rng.standard_normal(q.shape)
+    fd = (pr.grad(psi, q + h * vq, s, d, tau=tau)[0] - pr.grad(psi, q - h * vq, s, d, tau=tau)[0]) / (2 * h)
+    assert abs(fd - np.vdot(gq, vq).real) / abs(fd) < 1e-6
+
+
+def test_g_tau_reduces_to_f1_f2():
+    """G_tau at tau = 1 is F_1 (Eq. (10)) and at tau = 2 is F_2 (Eq. (9)), App. A.3 ("we retrieve the
+    main terms ... by setting tau equal to 2 and 1"): the general residual equals the two dedicated
+    branches (both pinned by finite differences above), also at w = 0 (reading C7)."""
+    rng = np.random.default_rng(32)
+    w = rng.standard_normal((8, 8)) + 1j * rng.standard_normal((8, 8))
+    w[0, 0] = 0
+    a = np.abs(rng.standard_normal((8, 8)))
+    F1, r1 = npo.residual_tau(w, a, 1.0)
+    m = np.abs(w)
+    assert abs(F1 - np.sum((m - a) ** 2)) < 1e-12 * F1
+    assert np.abs(r1 - np.where(m > 0, w - a * w / np.where(m > 0, m, 1), 0)).max() < 1e-13
+    F2, r2 = npo.residual_tau(w, a, 2.0)
+    assert abs(F2 - np.sum((m ** 2 - a ** 2) ** 2)) < 1e-12 * F2
+    assert np.abs(r2 - 2 * (m ** 2 - a ** 2) * w).max() < 1e-12
+
+
+@pytest.mark.parametrize("tau", [0.5, 1.5])
+def test_g_tau_reference_arm_finite_differences(tau):
+    """G_tau reference term in np_oracle.grad_ref: central differences vs Re<v, grad>."""
+    cfg = synth.CONFIGS["cfg4"]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    L, N, R = 32, 16, 2
+    rng = np.random.default_rng(33)
+    q = 1 + 0.2 * (rng.standard_normal((L, L)) + 1j * rng.standard_normal((L, L)))
+    rs = rng.uniform(-5, 5, size=(R, 2))
+    d = np.abs(rng.standard_normal((R, N, N)))
+    F, gq = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs, d, tau=tau)
+    h = 1e-6
+    v = rng.standard_normal(q.shape) + 1j * rng.standard_normal(q.shape)
+    Fp = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q + h * v, rs, d, False, tau=tau)[0]
+    Fm = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q - h * v, rs, d, False, tau=tau)[0]
+    fd = (Fp - Fm) / (2 * h)
+    assert abs(fd - np.vdot(gq, v).real) / abs(fd) < 1e-6
