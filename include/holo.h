@@ -128,6 +128,14 @@ holo_status holo_adj(holo_plan *p, const void *y /*[K][nz][n][n]*/, const void *
 #define HOLO_INTENSITY 4u      /* holo_grad: intensity objective F_2 (tau = 2, Eq. (9)):
                                   F = sum (|w|^2 - sqrt_d^2)^2, rho = 2 (|w|^2 - sqrt_d^2) w (App. A.3)  */
 
+/* Penalty exponent tau of the objective (App. A.3, Eq. (mintau)):
+ *   G_tau = sum_{k,j} || |w_kj|^tau - sqrt_d_kj^tau ||^2  (+ the same for the reference frames),
+ *   rho   = h'(|w|^2) w = tau (|w|^tau - sqrt_d^tau) |w|^(tau - 2) w   (0 where w = 0, reading C7),
+ * used by every later holo_grad / holo_grad_full / holo_grad_ref call on this plan (the gradient keeps
+ * Eq. (11)'s factor 2: grad = 2 L^* rho).  tau = 1 (default) is F_1 (Eq. (10)), tau = 2 is F_2
+ * (Eq. (9)).  HOLO_INTENSITY still selects tau = 2 for one call.  HOLO_EINVAL outside [0.25, 4]. */
+holo_status holo_set_tau(holo_plan *p, double tau);
+
 /* Fused sweep at (psi, q) over this plan's angles (O8-O12; Eqs. (10)-(12)).
  * Writes fp64 DEVICE scalars sc[3]:
  *   sc[0] = F_local = sum_{k,j} sum_pix (|w_kj| - sqrt_d_kj)^2                 (Eq. (10))

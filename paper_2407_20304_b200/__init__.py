@@ -99,6 +99,8 @@ _lib.holo_grad_full.restype = _S
 
 _lib.holo_set_gq_event.argtypes = [_P, _P]
 _lib.holo_set_gq_event.restype = _S
+_lib.holo_set_tau.argtypes = [_P, ctypes.c_double]
+_lib.holo_set_tau.restype = _S
 
 _lib.holo_profile_enable.argtypes = [_P, ctypes.c_int]
 _lib.holo_profile_enable.restype = _S
@@ -114,7 +116,7 @@ EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes"
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
             "holo_grad_ref", "holo_fwd_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
             "holo_profile_read", "holo_upsample2", "holo_bin2", "holo_init_probe", "holo_init_psi",
-            "holo_set_probe_shifts", "holo_grad_full", "holo_set_gq_event"]
+            "holo_set_probe_shifts", "holo_grad_full", "holo_set_gq_event", "holo_set_tau"]
 
 
 class HoloError(RuntimeError):
@@ -220,6 +222,10 @@ class Plan:
         event.record(self.stream)
         self._gq_event = event
         self._chk(_lib.holo_set_gq_event(self._h, ctypes.c_void_p(event.cuda_event)))
+
+    def set_tau(self, tau):
+        """holo_set_tau: penalty exponent of G_tau (App. A.3) for later grad calls (1 = F_1, 2 = F_2)."""
+        self._chk(_lib.holo_set_tau(self._h, float(tau)))
 
     def set_probe_shifts(self, s):
         """holo_set_probe_shifts: per-frame probe shifts s^p [K][nz][2] (None: plain q_j path)."""

@@ -33,7 +33,8 @@ struct holo_plan {
   float2 *T1 = nullptr, *Aw = nullptr, *W1 = nullptr, *V1 = nullptr, *T3 = nullptr, *G = nullptr, *QJ = nullptr;
   double *partF = nullptr, *partX3 = nullptr, *partQ = nullptr;
   int nbx2 = 0, nbx3 = 0;  // CTAs of one frame's X2 launch / one angle's X3 launch (partials per CTA)
-  int tau2 = 0;            // objective of the current call: 0 = F_1 (amplitude), 1 = F_2 (intensity)
+  float tau = 1.f;         // penalty exponent of the current call (G_tau, App. A.3): 1 = F_1, 2 = F_2
+  double tau_set = 1.0;    // holo_set_tau (HOLO_INTENSITY overrides it with 2 for one call)
   size_t ws_bytes = 0;
   std::vector<void *> allocs;
   std::vector<size_t> alloc_bytes;

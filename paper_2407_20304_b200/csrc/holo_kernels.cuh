@@ -87,6 +87,33 @@ __device__ __forceinline__ void red_add2(float2 *p, float2 v) {
   asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
 }
 
+// ---- residual of the penalty G_tau (App. A.3) ------------------------
+// h(phi) = (phi^{tau/2} - a^tau)^2 with phi = |w|^2, a = sqrt(d~):  F += h(|w|^2),
+// rho = h'(|w|^2) w = tau (|w|^tau - a^tau) |w|^{tau - 2} w  (the proposition's 2 L^*(H' . Lpsi)
+// carries the remaining factor 2 in the gradient).  tau = 1 is F_1 (Eq. (10)): rho = w - a w/|w|;
+// tau = 2 is F_2 (Eq. (9)): rho = 2 (|w|^2 - a^2) w.  rho = 0 where w = 0 (reading C7, all tau).
+// tau is uniform over the launch, so the branches do not diverge.
+__device__ __forceinline__ float2 residual_tau(float2 w, float a, float tau, double &acc) {
+  const float m2 = w.x * w.x + w.y * w.y;
+  if (tau == 1.0f) {
+    const float m = sqrtf(m2);
+    const float dm = m - a;
+    acc += (double)(dm * dm);
+    const float f = m > 0.f ? 1.0f - __fdividef(a, m) : 0.f;
+    return cscale(w, f);
+  }
+  if (tau == 2.0f) {
+    const float dm = m2 - a * a;
+    acc += (double)dm * (double)dm;
+    return cscale(w, 2.0f * dm);
+  }
+  const float wt = m2 > 0.f ? powf(m2, 0.5f * tau) : 0.f;  // |w|^tau
+  const float at = a > 0.f ? powf(a, tau) : 0.f;
+  const float dm = wt - at;
+  acc += (double)dm * (double)dm;
+  return m2 > 0.f ? cscale(w, tau * dm * (wt / m2)) : make_float2(0.f, 0.f);
+}
+
 // ---- layout-S line I/O ----------------------------------------------------------
 template <int L>
 __device__ __forceinline__ void ld_row(float2 (&v)[16], const float2 *__restrict__ row, int t) {

@@ -217,7 +217,7 @@ template <int L, int MODE>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x2(const float2 *__restrict__ in, size_t in_stride, const float *__restrict__ sqrt_d, size_t d_stride,
          float2 *__restrict__ out, size_t out_stride, double *__restrict__ partial, int part_stride, Tables tb,
-         const __grid_constant__ TabSeq seq, int N, int tau2) {
+         const __grid_constant__ TabSeq seq, int N, float tau) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
@@ -269,19 +269,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       const int c = t + r * T - o;
       float2 w = make_float2(0.f, 0.f);
       if (act && c >= 0 && c < N) {
-        const float d = dv[r];
-        const float m2 = v[r].x * v[r].x + v[r].y * v[r].y;
-        if (tau2) {  // F_2 (tau = 2, Eq. (9)): (|w|^2 - d~)^2, rho = h'(|w|^2) w = 2 (|w|^2 - d~) w
-          const float dm = m2 - d * d;
-          acc += (double)dm * (double)dm;
-          w = cscale(v[r], 2.0f * dm);
-        } else {  // F_1 (tau = 1, Eq. (10)): (|w| - sqrt d~)^2, rho = w - sqrt(d~) w/|w|, 0 at w = 0 (C7)
-          const float m = sqrtf(m2);
-          const float dm = m - d;
-          acc += (double)(dm * dm);
-          const float f = m > 0.f ? 1.0f - __fdividef(d, m) : 0.f;
-          w = cscale(v[r], f);
-        }
+        w = residual_tau(v[r], dv[r], tau, acc);  // G_tau (App. A.3): F_1 at tau = 1, F_2 at 2
       }
       v[r] = w;
     }

@@ -492,7 +492,7 @@ holo_status grad_impl(holo_plan *p, const void *psi, const void *q, const float 
   if (!q || !sc || (K > 0 && (!psi || !sqrt_d))) return fail(p, HOLO_EINVAL, "null pointer");
   const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0, acc = (flags & HOLO_ACCUMULATE_Q) != 0;
   const bool ref = sqrt_dref != nullptr && p->n_ref > 0;
-  p->tau2 = (flags & HOLO_INTENSITY) ? 1 : 0;
+  p->tau = (flags & HOLO_INTENSITY) ? 2.f : (float)p->tau_set;
   HC(cudaMemsetAsync(sc, 0, 3 * sizeof(double), p->stream));
   float2 *gq = obj ? nullptr : (float2 *)grad_q_part;
   if (K == 0) {  // empty shard: F = 0 and a zero probe-gradient partial (sums over no angles)
@@ -557,6 +557,14 @@ holo_status holo_set_gq_event(holo_plan *p, void *event) {
   return HOLO_OK;
 }
 
+holo_status holo_set_tau(holo_plan *p, double tau) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!(tau >= 0.25 && tau <= 4.0)) return fail(p, HOLO_EINVAL, "tau must lie in [0.25, 4]");
+  p->tau_set = tau;
+  return HOLO_OK;
+}
+
 holo_status holo_set_probe_shifts(holo_plan *p, const double *s) {
   holo_status st = precheck(p);
   if (st != HOLO_OK) return st;
@@ -603,7 +611,7 @@ holo_status holo_grad_ref(holo_plan *p, const void *q, const float *sqrt_dref, v
   if (!q || !sc || (p->n_ref > 0 && !sqrt_dref)) return fail(p, HOLO_EINVAL, "null pointer");
   HC(cudaMemsetAsync(sc, 0, sizeof(double), p->stream));
   const bool obj = (flags & HOLO_OBJECTIVE_ONLY) != 0, acc = (flags & HOLO_ACCUMULATE_Q) != 0;
-  p->tau2 = (flags & HOLO_INTENSITY) ? 1 : 0;
+  p->tau = (flags & HOLO_INTENSITY) ? 2.f : (float)p->tau_set;
   float2 *gq = obj ? nullptr : (float2 *)grad_q_part;
   if (p->n_ref == 0) {
     if (gq && !acc) HC(cudaMemsetAsync(gq, 0, sizeof(float2) * (size_t)p->L * p->L, p->stream));

@@ -242,7 +242,7 @@ template <int L, int MODE>
 __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     k_ref_rows(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
                double *__restrict__ partial, const float2 *__restrict__ Hx, const float4 *__restrict__ tw,
-               const float2 *__restrict__ tw3, int N, float scale, int accumulate, int tau2 = 0) {
+               const float2 *__restrict__ tw3, int N, float scale, int accumulate, float tau = 1.f) {
   using E = LineEng<L>;
   extern __shared__ float4 sm4[];
   __shared__ double red[32];
@@ -278,19 +278,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
       const int c = E::isp(st, r) - o;
       float2 w = make_float2(0.f, 0.f);
       if (act && c >= 0 && c < N) {
-        const float d = __ldg(sqrt_d + (size_t)y * N + c);
-        const float m2 = v[r].x * v[r].x + v[r].y * v[r].y;
-        if (tau2) {  // F_2 reference term (Eq. (9)): (|w|^2 - d~)^2, rho = 2 (|w|^2 - d~) w
-          const float dm = m2 - d * d;
-          acc += (double)dm * (double)dm;
-          w = cscale(v[r], 2.0f * dm);
-        } else {  // F_1: O9 / reading C7
-          const float m = sqrtf(m2);
-          const float dm = m - d;
-          acc += (double)(dm * dm);
-          const float f = m > 0.f ? 1.0f - __fdividef(d, m) : 0.f;
-          w = cscale(v[r], f);
-        }
+        w = residual_tau(v[r], __ldg(sqrt_d + (size_t)y * N + c), tau, acc);  // G_tau, App. A.3
       }
       v[r] = w;
     }

@@ -282,23 +282,23 @@ struct Run {
         pbeg(p);
         if (mode == 1) {
           k_x2<L, X2_FWD><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, nullptr, 0, wout + fo * NN, nz * NN, pf,
-                                                         nz * nbx2, tb, qh, N, p->tau2);
+                                                         nz * nbx2, tb, qh, N, p->tau);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
           continue;
         }
         if (mode == 3) {
           k_x2<L, X2_OBJ><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, sqrt_d + fo * NN, nz * NN, nullptr, 0, pf,
-                                                         nz * nbx2, tb, qh, N, p->tau2);
+                                                         nz * nbx2, tb, qh, N, p->tau);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8 / 2), nb * N * fl * 2);
           continue;
         }
         if (mode == 0) {
           k_x2<L, X2_GRAD><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, sqrt_d + fo * NN, nz * NN, p->V1, NL, pf,
-                                                          nz * nbx2, tb, qh, N, p->tau2);
+                                                          nz * nbx2, tb, qh, N, p->tau);
           pend(p, HOLO_PASS_X2, nb * (2 * rN * A + NN8 / 2), nb * N * fl * 4);
         } else {
           k_x2<L, X2_ADJ><<<g2, NT, SM::XT, p->stream>>>(yin + fo * NN, nz * NN, nullptr, 0, p->V1, NL, pf,
-                                                         nz * nbx2, tb, qh, N, p->tau2);
+                                                         nz * nbx2, tb, qh, N, p->tau);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
         }
         // ---- Y2 (batched): v = D_y^* V1[b]; G_j += conj(Aw[b]) v  (PS: Ut[b][j] = Hq_y^* FFT_y(conj(Aw) v));
@@ -461,7 +461,7 @@ struct RefRun {
       k_ref_r1b<L><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, tw3, N);
       k_ref_rows<L, REF_R2><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
                                                                       p->partR + (size_t)r0 * gn, H, tw, tw3, N, 1.f,
-                                                                      0, p->tau2);
+                                                                      0, p->tau);
       if (want_q) k_ref_r3b<L><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, tw3, N, f0);
       // bytes: Qhat once, W write + read, sqrt_d, V write + read per frame, Ghat once per batch
       pend(p, HOLO_PASS_REF,

@@ -269,3 +269,36 @@ def test_intensity_objective_f2_parity(name, K):
     p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, gpsi, gqd, flags=hb.HOLO_INTENSITY)
     assert abs(host(sc).real[0] - F) / F < TOL_S
     assert rel(host(gpsi), gp) < TOL_G and rel(host(gqd), gq) < TOL_G
+
+
+@pytest.mark.parametrize("name,K,tau", [("cfg0", 4, 1.5), ("cfg0", 4, 0.5), ("cfg1", 2, 3.0)])
+def test_g_tau_objective_parity(name, K, tau):
+    """holo_set_tau: the general penalty G_tau (App. A.3) and its gradients vs the numpy
+    oracle's residual_tau; setting tau back to 1 restores F_1 exactly as before."""
+    c = Case(name, K, oracle_kind="np")
+    p = make_plan(c.cfg, c.K)
+    p.set_shifts(c.s)
+    pr = npo.Problem(c.g, c.cfg.npad, c.cfg.n)
+    F, gp, gq = pr.grad(c.psi, c.q, c.s, c.d, tau=tau)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
+    p.set_tau(tau)
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, gpsi, gqd)
+    assert abs(host(sc).real[0] - F) / F < TOL_S
+    assert rel(host(gpsi), gp) < TOL_G and rel(host(gqd), gq) < TOL_G
+    p.set_tau(1.0)
+    F1, gp1, gq1 = pr.grad(c.psi, c.q, c.s, c.d)
+    p.grad(dev(c.psi), dev(c.q), dev(c.d, torch.float32), sc, None, gpsi, gqd)
+    assert abs(host(sc).real[0] - F1) / F1 < TOL_S
+    assert rel(host(gpsi), gp1) < TOL_G and rel(host(gqd), gq1) < TOL_G
+
+
+def test_set_tau_rejects_out_of_range():
+    import paper_2407_20304_b200 as hb
+    c = synth.CONFIGS["cfg0"]
+    p = make_plan(c, 1)
+    for bad in (0.0, -1.0, 5.0, float("nan")):
+        with pytest.raises(hb.HoloError):
+            p.set_tau(bad)
+    p.set_tau(2.0)

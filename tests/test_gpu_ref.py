@@ -144,3 +144,22 @@ def test_ref_arm_f2_parity():
     Fg, gg = run_gpu(p, q, d, flags=hb.HOLO_INTENSITY)
     assert abs(Fg - F) / F < TOL_S
     assert rel(gg, gq) < TOL_G
+
+
+@pytest.mark.parametrize("tau", [0.5, 1.5])
+def test_ref_arm_g_tau_parity(tau):
+    """holo_set_tau on the reference arm: G_tau reference term and its q-gradient (App. A.3)."""
+    cfg = synth.CONFIGS["cfg4"]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    L, N, R = 256, 128, 3
+    q_t = synth.probe(cfg, L=L).numpy()
+    rs = np.random.default_rng(19).uniform(-8, 8, size=(R, 2))
+    d = ref_data(g, q_t, rs, N, 19)
+    q = 0.9 * q_t
+    F, gq = npo.grad_ref(g.wavelength, g.p0, g.zeta[0], q, rs, d, tau=tau)
+    p = plan(cfg, L, N)
+    p.set_ref_shifts(rs)
+    p.set_tau(tau)
+    Fg, gg = run_gpu(p, q, d)
+    assert abs(Fg - F) / F < TOL_S
+    assert rel(gg, gq) < TOL_G
