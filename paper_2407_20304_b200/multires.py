@@ -1,4 +1,4 @@
-"""Multiresolution schedule.
+"""Multiresolution schedule and probe-subset updates.
 
 The paper starts the joint reconstruction on 8x8-binned data, then 4x4, 2x2 and full
 resolution, "extrapolat[ing] the recovered object with the probe function to a grid twice
@@ -75,3 +75,42 @@ def run_schedule(levels, sqrt_d, shifts, n, npad, z1, wavelength, Z, detector_pi
         psi, q = cg.psi, cg.q
         del cg, plan
     return psi, q, hist
+
+
+# ---------------------------------------------------------------------------------- probe subset
+def probe_subset_indices(K, n_sub):
+    """n_sub angles spread evenly over [0, K) ("the probe can be approximated by considering
+    only a limited set of projections ... 20-50 projections"): round(i K / n_sub), i < n_sub."""
+    n_sub = max(1, min(int(n_sub), K))
+    return np.unique(np.floor(np.arange(n_sub) * K / n_sub + 0.5).astype(np.int64).clip(0, K - 1))
+
+
+def run_probe_subset(sqrt_d, shifts, psi0, q0, n_sub, iters_probe, iters_object, make_plan,
+                     rho_psi=1.0, rho_q=None, distributed=None):
+    """Probe-subset schedule (reading R6 of P:257): stage 1 runs the joint psi/q CG on the n_sub
+    angles of probe_subset_indices only (their psi and the shared probe q); stage 2 freezes q
+    (rho_q = 0: no probe-gradient work) and runs object-only CG over all K angles, starting from
+    psi0 with the subset angles replaced by their stage-1 result.  make_plan(idx) -> a plan whose
+    angles are idx (shifts set); stage 1's plan is released before stage 2's is made.
+    Returns (psi, q, history) with history = [stage-1 dict, stage-2 dict]."""
+    K = sqrt_d.shape[0]
+    idx = probe_subset_indices(K, n_sub)
+    sel = torch.as_tensor(idx, device=sqrt_d.device)
+    plan = make_plan(idx)
+    cg = JointCG(plan, sqrt_d.index_select(0, sel).contiguous(), psi0.index_select(0, sel).contiguous(), q0,
+                 rho_psi=rho_psi, rho_q=(1.0 / len(idx) if rho_q is None else rho_q), distributed=distributed)
+    hist = [dict(stage="probe", angles=[int(i) for i in idx], F_start=cg.start())]
+    for _ in range(iters_probe):
+        cg.iterate()
+    hist[0].update(F_end=cg.F, iterations=iters_probe, sweeps=cg.sweeps)
+    q = cg.q.clone()
+    psi = psi0.clone()
+    psi.index_copy_(0, sel, cg.psi)
+    del cg, plan
+    plan = make_plan(np.arange(K))
+    cg = JointCG(plan, sqrt_d, psi, q, rho_psi=rho_psi, rho_q=0.0, distributed=distributed)
+    hist.append(dict(stage="object", angles=K, F_start=cg.start()))
+    for _ in range(iters_object):
+        cg.iterate()
+    hist[1].update(F_end=cg.F, iterations=iters_object, sweeps=cg.sweeps)
+    return cg.psi, cg.q, hist

@@ -34,6 +34,10 @@ class JointCG:
         # holo_grad_full when the plan provides it (the CPU test double of the dist tests does not)
         self.fused = hasattr(plan, "grad_full") if fused is None else bool(fused)
         self.rho = (float(rho_psi), float(rho_q))
+        # rho_q = 0 freezes the probe (object-only CG, e.g. the second stage of the probe-subset
+        # schedule): no probe-gradient work in the library (grad_q_part = NULL skips the
+        # Aw stores and the G_j accumulation), no g_q exchange, q never moves.
+        self.q_frozen = self.rho[1] == 0.0
         self.gamma_init, self.max_halvings = float(gamma_init), int(max_halvings)
         self.group = group
         self.dist = dist.is_available() and dist.is_initialized() if distributed is None else distributed
@@ -66,6 +70,8 @@ class JointCG:
         """F and grad at (psi, q); returns host (F, gg_psi, geta_psi, gg_q, geta_q)."""
         p = self.plan
         sc3 = self.sc[:3]
+        if self.q_frozen:
+            g_q = None
         # always called, also on a rank without angles: the library then writes F = 0 and a ZERO
         # probe-gradient partial, so no stale (already reduced) g_q enters the allreduce.
         if self.dref is None:
@@ -76,7 +82,9 @@ class JointCG:
             p.grad(psi, q, self.d, sc3, eta_psi, g_psi, g_q)
             p.grad_ref(q, self.dref, self.scr, g_q, flags=HOLO_ACCUMULATE_Q)
             sc3[:1] += self.scr
-        if self.dist:
+        if self.dist and g_q is None:
+            dist.all_reduce(sc3, group=self.group)
+        elif self.dist:
             # exchange 1: probe-gradient partial (complex64 viewed as float32), exchange 2: scalars.
             # With an overlap event (CUDA/NCCL), exchange 1 runs on a side stream that waits only for
             # the event the library records as soon as g_q is complete, i.e. while the last angle
@@ -90,7 +98,10 @@ class JointCG:
             else:
                 dist.all_reduce(torch.view_as_real(g_q), group=self.group)
                 dist.all_reduce(sc3, group=self.group)
-        p.q_dots(g_q, eta_q, self.sc[3:])
+        if g_q is None:
+            self.sc[3:].zero_()
+        else:
+            p.q_dots(g_q, eta_q, self.sc[3:])
         s = self.sc.cpu().tolist()  # the single host sync of the sweep
         self.sweeps += 1
         if not math.isfinite(s[0]):
@@ -116,12 +127,13 @@ class JointCG:
         if forced_gamma is not None:
             gamma = float(forced_gamma)
         cin = HoloCgIn(self.gPg(), self.g_eta, self.gprev_eta, gamma, self.rho[0], self.rho[1], int(first), 0)
-        out = p.cg_step(cin, self.psi, self.eta_psi, self.g_psi, self.psi_t, self.q, self.eta_q, self.g_q, self.q_t)
+        qb = (None,) * 4 if self.q_frozen else (self.q, self.eta_q, self.g_q, self.q_t)
+        out = p.cg_step(cin, self.psi, self.eta_psi, self.g_psi, self.psi_t, *qb)
         g_eta_new = out.g_eta_new
         accepted = False
         tries = 0
         while True:
-            s = self.sweep(self.psi_t, self.q_t, self.eta_psi, self.eta_q, self.gt_psi, self.gt_q)
+            s = self.sweep(self.psi_t, self.q if self.q_frozen else self.q_t, self.eta_psi, self.eta_q, self.gt_psi, self.gt_q)
             tries += 1
             if forced_gamma is not None or s[0] < self.F:
                 accepted = True
@@ -130,10 +142,12 @@ class JointCG:
                 break
             gamma *= 0.5
             cin = HoloCgIn(0.0, 0.0, 0.0, gamma, self.rho[0], self.rho[1], 0, 1)
-            p.cg_step(cin, self.psi, self.eta_psi, None, self.psi_t, self.q, self.eta_q, None, self.q_t)
+            qb = (None,) * 4 if self.q_frozen else (self.q, self.eta_q, None, self.q_t)
+            p.cg_step(cin, self.psi, self.eta_psi, None, self.psi_t, *qb)
         if accepted:
             self.psi, self.psi_t = self.psi_t, self.psi
-            self.q, self.q_t = self.q_t, self.q
+            if not self.q_frozen:
+                self.q, self.q_t = self.q_t, self.q
             self.g_psi, self.gt_psi = self.gt_psi, self.g_psi
             self.g_q, self.gt_q = self.gt_q, self.g_q
             self.F, self.dots = s[0], s

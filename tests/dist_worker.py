@@ -39,7 +39,8 @@ class FakePlan:
         sc[1] = float(np.vdot(gp, gp).real)
         sc[2] = float(np.vdot(eta_psi_prev.numpy(), gp).real) if eta_psi_prev is not None else 0.0
         grad_psi.copy_(torch.from_numpy(gp))
-        grad_q_part.copy_(torch.from_numpy(gq))
+        if grad_q_part is not None:  # NULL: no probe gradient (include/holo.h)
+            grad_q_part.copy_(torch.from_numpy(gq))
 
     def grad_ref(self, q, sqrt_dref, sc, grad_q_part=None, flags=0):
         F, gq = oracle.grad_ref(self.g, q.numpy(), self.rs, sqrt_dref.numpy())

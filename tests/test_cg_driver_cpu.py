@@ -86,3 +86,42 @@ def test_joint_cg_driver_forced_gamma_matches_oracle():
         assert abs(a["F"] - b["F"]) <= 1e-12 * b["F"]
         assert abs(a["beta"] - b["beta"]) <= 1e-12 * max(abs(b["beta"]), 1e-12)
     assert np.linalg.norm(cg.q.numpy() - x_or[1]) <= 1e-12 * np.linalg.norm(x_or[1])
+
+
+def test_probe_subset_schedule_reproduces_oracle():
+    """Probe-subset schedule (reading R6): multires.run_probe_subset over the fp64 test
+    double equals O13 run twice -- joint CG on the subset angles, then CG with P = diag(1, 0)
+    (probe frozen) over all angles -- F histories, final psi and q (q bitwise unchanged in stage 2)."""
+    from paper_2407_20304_b200.multires import probe_subset_indices, run_probe_subset
+    cfg, g, psi_t, q_t, s, d = _problem(K=4)
+    K = psi_t.shape[0]
+    idx = probe_subset_indices(K, 2)
+    assert list(idx) == [0, 2]
+    assert list(probe_subset_indices(180, 20)) == [int(np.floor(i * 9 + 0.5)) for i in range(20)]
+    assert list(probe_subset_indices(3, 50)) == [0, 1, 2]
+    psi0, q0 = np.ones_like(psi_t), 0.9 * q_t
+    n1, n2 = 3, 3
+
+    def sweep_sub(x):
+        F, gp, gq = oracle.grad(g, x[0], x[1], s[idx], d[idx])
+        return F, [gp, gq]
+
+    x1, h1 = ocg.run(sweep_sub, [psi0[idx], q0], (1.0, 1.0 / len(idx)), n1)
+    psi_mid = psi0.copy()
+    psi_mid[idx] = x1[0]
+
+    def sweep_all(x):
+        F, gp, gq = oracle.grad(g, x[0], x[1], s, d)
+        return F, [gp, gq]
+
+    x2, h2 = ocg.run(sweep_all, [psi_mid, x1[1]], (1.0, 0.0), n2)
+    assert np.array_equal(x2[1], x1[1])
+
+    psi, q, hist = run_probe_subset(torch.from_numpy(d.copy()), s, torch.from_numpy(psi0.copy()),
+                                    torch.from_numpy(q0.copy()), 2, n1, n2,
+                                    make_plan=lambda ii: FakePlan(g, s[np.asarray(ii)]), distributed=False)
+    assert abs(hist[0]["F_end"] - h1[-1]["F"]) <= 1e-12 * h1[-1]["F"]
+    assert abs(hist[1]["F_end"] - h2[-1]["F"]) <= 1e-12 * h2[-1]["F"]
+    assert hist[1]["F_end"] <= hist[1]["F_start"]
+    assert np.abs(q.numpy() - x1[1]).max() <= 1e-12 * np.abs(x1[1]).max()
+    assert np.abs(psi.numpy() - x2[0]).max() <= 1e-10 * np.abs(x2[0]).max()

@@ -87,3 +87,59 @@ def test_schedule_two_levels():
     # the fine level starts from the upsampled coarse fit, better than psi = 1 with the upsampled q0
     F_naive = pr.grad(np.ones_like(psi_t), npo.upsample2(qc), s, d)[0]
     assert hist[1]["F_start"] < F_naive
+
+
+def test_object_only_sweep_parity():
+    """rho_q = 0 path (probe frozen): holo_grad with grad_q_part = NULL gives the oracle's F and
+    grad_psi (cfg0, 4 angles) -- the probe-gradient work is skipped, nothing else changes."""
+    cfg = synth.CONFIGS["cfg0"]
+    K = 4
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    psi_t, q_t, s = synth.psi_stack(cfg, K=K).numpy(), synth.probe(cfg).numpy(), synth.shifts(cfg, K=K)
+    d = synth.poisson_amplitude(np.abs(oracle.fwd(g, psi_t, q_t, s, cfg.n)) ** 2, cfg.photons, cfg)
+    psi, q = np.ones_like(psi_t), 0.9 * q_t
+    F, gp, _ = oracle.grad(g, psi, q, s, d)
+    import paper_2407_20304_b200 as hb
+    p = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=0)
+    p.set_shifts(s)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(K, cfg.npad, cfg.npad, dtype=torch.complex64, device="cuda")
+    p.grad(dev(psi), dev(q), dev(d, torch.float32), sc, None, gpsi, None)
+    torch.cuda.synchronize()
+    assert abs(float(sc[0]) - F) / F < 1e-4
+    assert rel(gpsi.cpu().numpy(), gp) < 1e-4
+
+
+def test_probe_subset_schedule():
+    """Probe-subset schedule (reading R6) on the GPU, cfg1 geometry at 256^2 (8 angles,
+    subset of 3): stage 1 (joint CG on the subset) and stage 2 (object-only CG on all angles) each
+    lower F, the plans hold the evenly spread subset and then all angles, and the final state's
+    F is the oracle's F there (the CPU test pins the driver to O13 step by step)."""
+    import paper_2407_20304_b200 as hb
+    from paper_2407_20304_b200.multires import run_probe_subset
+    cfg = synth.CONFIGS["cfg1"]
+    K, L, N = 8, 256, 128
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    psi_t = synth.psi_stack(cfg, K=K, L=L).numpy()
+    q_t = synth.probe(cfg, L=L).numpy()
+    s = np.random.default_rng(5).uniform(-2, 2, size=(K, cfg.nz, 2))
+    pr = npo.Problem(g, L, N)
+    out = pr.fwd(psi_t, q_t, s)
+    d = np.stack([np.stack([np.abs(out[(k, j)]) for j in range(cfg.nz)]) for k in range(K)])
+    psi0, q0 = np.ones_like(psi_t), 0.9 * q_t
+    seen = {}
+
+    def make_plan(idx):
+        p = hb.Plan(N, L, cfg.z1, len(idx), cfg.wavelength, cfg.Z, cfg.det_pixel, device=0, angle_batch=4)
+        p.set_shifts(s[np.asarray(idx)])
+        seen.setdefault("idx", []).append(np.asarray(idx).copy())
+        return p
+
+    psi, q, hist = run_probe_subset(dev(d, torch.float32), s, dev(psi0), dev(q0), 3, 4, 4, make_plan)
+    assert [list(i) for i in seen["idx"]] == [[0, 3, 5], list(range(K))]
+    for h in hist:
+        assert h["F_end"] < h["F_start"], h
+    # the final state's F (stage 2 never moved q) is the oracle's F there
+    q1 = q.cpu().numpy().astype(np.complex128)
+    F_end = pr.grad(psi.cpu().numpy().astype(np.complex128), q1, s, d)[0]
+    assert abs(F_end - hist[1]["F_end"]) / F_end < 1e-4
