@@ -425,3 +425,77 @@ __device__ __forceinline__ void fft(float2 (&v)[16], Xch &x, const int t, const 
 }
 
 }  // namespace holo
+
+namespace holo {
+
+// ---- NV independent lines per thread (the 6144 = 3 x 2048 engine of holo_ref.cuh) -------------
+// Thread t holds NV lines of length L in layout S, line s in v[16 s .. 16 s + 15].  The NV
+// transforms run stage by stage in lockstep, so each exchange is ONE barrier pair for all NV lines
+// (their buffers at buf + s * bstride) and the butterflies of one line overlap the shared-memory
+// traffic of another.  Every thread of the CTA must call it (CTA barriers).
+template <int L, bool INV, int NV, int ST>
+__device__ __forceinline__ void r16_stage_nv(float2 (&v)[NV * 16], float2 *buf, int bstride, const int t,
+                                             const float4 *__restrict__ tw) {
+  using S = Shape<L>;
+  constexpr int Ns = S::F * pow16(ST);
+  constexpr int ROW0 = S::F * (pow16(ST) - 1) / 15;
+  const int m = t & (Ns - 1);
+  {
+    const float4 a = __ldg(tw + 2 * (ROW0 + m)), b = __ldg(tw + 2 * (ROW0 + m) + 1);
+    const float2 w1 = make_float2(a.x, a.y), w2 = make_float2(a.z, a.w), w4 = make_float2(b.x, b.y),
+                 w8 = make_float2(b.z, b.w);
+#pragma unroll
+    for (int s = 0; s < NV; s++) dft16_dit_tw<INV>(v + 16 * s, w1, w2, w4, w8);
+  }
+  if constexpr (ST + 1 < S::S16) {
+    const int base = (t - m) * 16 + m;
+    __syncthreads();  // the previous exchange's readers are done with buf
+#pragma unroll
+    for (int s = 0; s < NV; s++)
+#pragma unroll
+      for (int q = 0; q < 16; q++) buf[s * bstride + P(base + q * Ns)] = v[16 * s + q];
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < NV; s++)
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[16 * s + r] = buf[s * bstride + P(t + r * S::T)];
+    r16_stage_nv<L, INV, NV, ST + 1>(v, buf, bstride, t, tw);
+  }
+}
+
+template <int L, bool INV, int NV>
+__device__ __forceinline__ void fft_nv(float2 (&v)[NV * 16], float2 *buf, int bstride, const int t,
+                                       const float4 *__restrict__ tw) {
+  using S = Shape<L>;
+  constexpr int F = S::F, PER = S::PER;
+#pragma unroll
+  for (int s = 0; s < NV; s++) {
+#pragma unroll
+    for (int b = 0; b < PER; b++) {
+      float2 u[F];
+#pragma unroll
+      for (int k = 0; k < F; k++) u[k] = v[16 * s + b + PER * k];
+      if constexpr (F == 16 && HOLO_DIT)
+        dft16_dit<INV>(u);
+      else
+        dft_reg<F, INV>(u);
+#pragma unroll
+      for (int k = 0; k < F; k++) v[16 * s + b + PER * k] = u[k];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < NV; s++)
+#pragma unroll
+    for (int b = 0; b < PER; b++)
+#pragma unroll
+      for (int k = 0; k < F; k++) buf[s * bstride + P((t + S::T * b) * F + k)] = v[16 * s + b + PER * k];
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < NV; s++)
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[16 * s + r] = buf[s * bstride + P(t + r * S::T)];
+  r16_stage_nv<L, INV, NV, 0>(v, buf, bstride, t, tw);
+}
+
+}  // namespace holo

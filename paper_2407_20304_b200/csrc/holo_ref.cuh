@@ -14,10 +14,8 @@
 //
 // Line engines: power-of-two tori use the register-resident Stockham engine
 // (layout S in both domains).  N_p = 6144 = 3 * 2048 (configs[4], reading C16) uses
-// LineEng<6144>: three interleaved 2048-point sub-transforms of the decimated
-// sequences x[3n + s] (128 threads each) and one radix-3 combine through shared memory:
-//   spatial  register r of thread (g3, t)  <->  element 3 (t + 128 r) + g3
-//   spectral register r of thread (g3, t)  <->  element t + 128 r + 2048 g3
+// LineEng<6144>: each thread runs the three 2048-point sub-transforms of the decimated
+// sequences x[3n + s] in lockstep and combines them with a radix-3 step in registers:
 //   X[k + 2048 m] = sum_s W_3^{s m} W_6144^{s k} FFT_2048(x[3 . + s])[k].
 #pragma once
 #include "holo_kernels.cuh"
@@ -27,8 +25,9 @@ namespace holo {
 template <int L>
 struct LineEng {  // power of two: the Stockham engine, G lines per 512-thread CTA
   using C = Cta<L, 512>;
-  static constexpr int NT = 512, G = C::G, T = L / 16;
-  static constexpr size_t SMEM = C::XBYTES;
+  static constexpr int NT = 512, G = C::G, T = L / 16, R = 16, MINB = 1, MINB_ACC = 1;
+  static constexpr bool HOLD_SMEM = false;  // R1B / R3B keep their second line in registers
+  static constexpr size_t SMEM = C::XBYTES, SMEM_ACC = SMEM;
   struct St {
     Xch x;
     int t, g;
@@ -36,74 +35,71 @@ struct LineEng {  // power of two: the Stockham engine, G lines per 512-thread C
   __device__ __forceinline__ static St init(float2 *sm) { return St{C::xch(sm), C::t(), C::g()}; }
   __device__ __forceinline__ static int isp(const St &s, int r) { return s.t + r * T; }
   __device__ __forceinline__ static int ifr(const St &s, int r) { return s.t + r * T; }
-  __device__ __forceinline__ static void fwd(float2 (&v)[16], St &s, const float4 *tw, const float2 *) {
+  __device__ __forceinline__ static void fwd(float2 (&v)[R], St &s, const float4 *tw, const float2 *) {
     fft<L, false>(v, s.x, s.t, tw);
   }
-  __device__ __forceinline__ static void inv(float2 (&v)[16], St &s, const float4 *tw, const float2 *) {
+  __device__ __forceinline__ static void inv(float2 (&v)[R], St &s, const float4 *tw, const float2 *) {
     fft<L, true>(v, s.x, s.t, tw);
   }
 };
 
+// N_p = 6144 = 3 x 2048 (configs[4]): ONE line per 128-thread CTA, each thread holding the three
+// decimated sub-lines x[3 n + s] (s = 0, 1, 2) of 2048 points in layout S (48 values, v[16 s + r]):
+//   spatial  value (s, r) of thread t  <->  element 3 (t + 128 r) + s   (a thread's three values are
+//            adjacent: 24 contiguous bytes, a warp covers 768 contiguous bytes per r)
+//   spectral value (m, r) of thread t  <->  element t + 128 r + 2048 m
+// The three 2048-point sub-transforms run in lockstep (fft_nv: one barrier pair per exchange for
+// all three) and the radix-3 combine X[k + 2048 m] = sum_s W_3^{s m} W_6144^{s k} Y_s[k] is done in
+// registers (no third exchange).  Several CTAs per SM, so one CTA's exchange overlaps another's
+// butterflies.
 template <>
 struct LineEng<6144> {
-  static constexpr int L = 6144, LS = 2048, NT = 384, G = 1, T = 128;
-  using CS = Cta<LS, 128>;  // one 2048-point sub-line per 128 threads
-  static constexpr int GS = CS::GS;
-  static constexpr size_t SMEM = sizeof(float2) * (size_t)GS * 3;
-  static_assert(3 * GS >= 3 * LS, "radix-3 buffer must fit in the exchange space");
+  static constexpr int L = 6144, LS = 2048, NT = 128, G = 1, T = 128, R = 48;
+  static constexpr int MINB = 3;      // CTAs per SM of the plain passes (<= 170 registers)
+  static constexpr int MINB_ACC = 2;  // R1B / R3B keep a second 48-value line (Qhat column / Ghat sum)
+  static constexpr int BS = Shape<LS>::LP;  // one sub-line's exchange buffer (float2)
+  static constexpr size_t SMEM = sizeof(float2) * (size_t)BS * 3;
+  // R1B / R3B: the second line (Qhat column / batch sum) in a thread-private shared-memory slot
+  // behind the exchange buffers (value i of thread t at SMEM + 8 (i NT + t): conflict free)
+  static constexpr bool HOLD_SMEM = true;
+  static constexpr size_t SMEM_ACC = SMEM + sizeof(float2) * (size_t)R * NT;
   struct St {
-    Xch x;
-    int t, g, g3;
     float2 *buf;
+    int t, g;
   };
-  __device__ __forceinline__ static St init(float2 *sm) {
-    const int g3 = threadIdx.x / 128, t = threadIdx.x % 128;
-    return St{Xch{sm + (size_t)g3 * GS, 0, CS::LPB, g3}, t, 0, g3, sm};  // sub-line g3 = warps 4 g3 .. 4 g3 + 3
-  }
-  __device__ __forceinline__ static int isp(const St &s, int r) { return 3 * (s.t + r * T) + s.g3; }
-  __device__ __forceinline__ static int ifr(const St &s, int r) { return s.t + r * T + LS * s.g3; }
-  // radix-3 buffer slot of element k of sub-sequence m (padded like the engine)
-  __device__ __forceinline__ static int B(int m, int k) { return m * GS + P(k); }
-  // tw3[(g3 - 1) * 2048 + k] = W_6144^{g3 k} = e^{-2 pi i g3 k / 6144}, g3 = 1, 2
-  __device__ __forceinline__ static void fwd(float2 (&v)[16], St &s, const float4 *tw, const float2 *tw3) {
-    fft<LS, false>(v, s.x, s.t, tw);
-    if (s.g3) {
-#pragma unroll
-      for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(tw3 + (s.g3 - 1) * LS + s.t + r * T));
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 16; r++) s.buf[B(s.g3, s.t + r * T)] = v[r];
-    __syncthreads();
+  __device__ __forceinline__ static St init(float2 *sm) { return St{sm, (int)threadIdx.x, 0}; }
+  __device__ __forceinline__ static int isp(const St &s, int i) { return 3 * (s.t + (i & 15) * T) + (i >> 4); }
+  __device__ __forceinline__ static int ifr(const St &s, int i) { return s.t + (i & 15) * T + LS * (i >> 4); }
+  // tw3[(s - 1) * 2048 + k] = W_6144^{s k} = e^{-2 pi i s k / 6144}, s = 1, 2
+  __device__ __forceinline__ static void fwd(float2 (&v)[R], St &s, const float4 *tw, const float2 *tw3) {
+    fft_nv<LS, false, 3>(v, s.buf, BS, s.t, tw);
     constexpr float C3 = -0.5f, S3 = 0.86602540378443864676f;  // W_3 = e^{-2 pi i / 3} = C3 - i S3
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const int k = s.t + r * T;
-      const float2 y0 = s.buf[B(0, k)], y1 = s.buf[B(1, k)], y2 = s.buf[B(2, k)];
+      const float2 y0 = v[r], y1 = cmul(v[16 + r], ldg2(tw3 + k)), y2 = cmul(v[32 + r], ldg2(tw3 + LS + k));
       const float2 a = cadd(y1, y2), d = csub(y1, y2);
-      const float2 base = make_float2(y0.x + C3 * a.x, y0.y + C3 * a.y);
+      const float2 base = make_float2(fmaf(C3, a.x, y0.x), fmaf(C3, a.y, y0.y));
       const float2 rot = make_float2(S3 * d.y, -S3 * d.x);  // -i S3 (y1 - y2)
-      v[r] = s.g3 == 0 ? cadd(y0, a) : (s.g3 == 1 ? cadd(base, rot) : csub(base, rot));
+      v[r] = cadd(y0, a);
+      v[16 + r] = cadd(base, rot);
+      v[32 + r] = csub(base, rot);
     }
   }
-  __device__ __forceinline__ static void inv(float2 (&v)[16], St &s, const float4 *tw, const float2 *tw3) {
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 16; r++) s.buf[B(s.g3, s.t + r * T)] = v[r];
-    __syncthreads();
+  __device__ __forceinline__ static void inv(float2 (&v)[R], St &s, const float4 *tw, const float2 *tw3) {
     constexpr float C3 = -0.5f, S3 = 0.86602540378443864676f;  // conj(W_3) = C3 + i S3
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const int k = s.t + r * T;
-      const float2 x0 = s.buf[B(0, k)], x1 = s.buf[B(1, k)], x2 = s.buf[B(2, k)];
+      const float2 x0 = v[r], x1 = v[16 + r], x2 = v[32 + r];
       const float2 a = cadd(x1, x2), d = csub(x1, x2);
-      const float2 base = make_float2(x0.x + C3 * a.x, x0.y + C3 * a.y);
+      const float2 base = make_float2(fmaf(C3, a.x, x0.x), fmaf(C3, a.y, x0.y));
       const float2 rot = make_float2(-S3 * d.y, S3 * d.x);  // +i S3 (x1 - x2)
-      float2 y = s.g3 == 0 ? cadd(x0, a) : (s.g3 == 1 ? cadd(base, rot) : csub(base, rot));
-      if (s.g3) y = cmulc(y, ldg2(tw3 + (s.g3 - 1) * LS + k));
-      v[r] = y;
+      v[r] = cadd(x0, a);
+      v[16 + r] = cmulc(cadd(base, rot), ldg2(tw3 + k));
+      v[32 + r] = cmulc(csub(base, rot), ldg2(tw3 + LS + k));
     }
-    fft<LS, true>(v, s.x, s.t, tw);
+    fft_nv<LS, true, 3>(v, s.buf, BS, s.t, tw);
   }
 };
 
@@ -115,7 +111,7 @@ enum { REF_QHAT = 0, REF_R1 = 1, REF_R2 = 2, REF_R3 = 3, REF_FINAL = 4, REF_FWD 
 // R3   : v = pad(V col) -> forward along y -> x conj(Hy) -> Ghat (+)= v (P2)
 // FINAL: Ghat col -> inverse along y -> Ghat (P2, spatial y), in place
 template <int L, int MODE>
-__global__ void __launch_bounds__(LineEng<L>::NT, 1)
+__global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
     k_ref_cols(const float2 *__restrict__ in, float2 *__restrict__ out, const float2 *__restrict__ Hy,
                const float4 *__restrict__ tw, const float2 *__restrict__ tw3, int N, int first) {
   using E = LineEng<L>;
@@ -123,34 +119,34 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
   typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
   const int col = blockIdx.x * E::G + st.g;
   const int o = (L - N) / 2;
-  float2 v[16];
+  float2 v[E::R];
   if (MODE == REF_QHAT) {
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = ldg2(in + p2(E::isp(st, r), col, L));
+    for (int r = 0; r < E::R; r++) v[r] = ldg2(in + p2(E::isp(st, r), col, L));
     E::fwd(v, st, tw, tw3);
 #pragma unroll
-    for (int r = 0; r < 16; r++) out[p2(E::ifr(st, r), col, L)] = v[r];
+    for (int r = 0; r < E::R; r++) out[p2(E::ifr(st, r), col, L)] = v[r];
   } else if (MODE == REF_R1) {
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int f = E::ifr(st, r);
       v[r] = cmul(ldg2(in + p2(f, col, L)), ldg2(Hy + f));
     }
     E::inv(v, st, tw, tw3);
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int row = E::isp(st, r) - o;
       if (row >= 0 && row < N) out[p2(row, col, N)] = v[r];
     }
   } else if (MODE == REF_R3) {
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int row = E::isp(st, r) - o;
       v[r] = (row >= 0 && row < N) ? ldg2(in + p2(row, col, N)) : make_float2(0.f, 0.f);
     }
     E::fwd(v, st, tw, tw3);
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int f = E::ifr(st, r);
       const float2 a = cmulc(v[r], ldg2(Hy + f));
       float2 *p = out + p2(f, col, L);
@@ -158,10 +154,10 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     }
   } else {  // FINAL
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = in[p2(E::ifr(st, r), col, L)];
+    for (int r = 0; r < E::R; r++) v[r] = in[p2(E::ifr(st, r), col, L)];
     E::inv(v, st, tw, tw3);
 #pragma unroll
-    for (int r = 0; r < 16; r++) out[p2(E::isp(st, r), col, L)] = v[r];
+    for (int r = 0; r < E::R; r++) out[p2(E::isp(st, r), col, L)] = v[r];
   }
 }
 
@@ -169,7 +165,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
 // B_r reference frames per launch; frame b's tables at Href + 2 L b (x row, then y row).
 // R1B: the Qhat column is read ONCE; per frame: x Hy_b, inverse along y, rows [o, o+N) -> W_b
 template <int L>
-__global__ void __launch_bounds__(LineEng<L>::NT, 1)
+__global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
     k_ref_r1b(const float2 *__restrict__ Qhat, float2 *__restrict__ W, const float2 *__restrict__ Href, int nb,
               const float4 *__restrict__ tw, const float2 *__restrict__ tw3, int N) {
   using E = LineEng<L>;
@@ -177,19 +173,23 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
   typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
   const int col = blockIdx.x * E::G + st.g;
   const int o = (L - N) / 2;
-  float2 q0[16];
+  float2 q0[E::HOLD_SMEM ? 1 : E::R];
+  float2 *hold = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sm4) + E::SMEM) + threadIdx.x;
 #pragma unroll
-  for (int r = 0; r < 16; r++) q0[r] = ldg2(Qhat + p2(E::ifr(st, r), col, L));
+  for (int r = 0; r < E::R; r++) {
+    const float2 a = ldg2(Qhat + p2(E::ifr(st, r), col, L));
+    if constexpr (E::HOLD_SMEM) hold[r * E::NT] = a; else q0[r] = a;
+  }
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *Hy = Href + (size_t)b * 2 * L + L;
-    float2 v[16];
+    float2 v[E::R];
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = cmul(q0[r], ldg2(Hy + E::ifr(st, r)));
+    for (int r = 0; r < E::R; r++) v[r] = cmul(E::HOLD_SMEM ? hold[r * E::NT] : q0[r], ldg2(Hy + E::ifr(st, r)));
     E::inv(v, st, tw, tw3);
     float2 *w = W + (size_t)b * N * L;
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int row = E::isp(st, r) - o;
       if (row >= 0 && row < N) w[p2(row, col, N)] = v[r];
     }
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
 // R3B: per frame: pad(V_b col) -> forward along y -> x conj(Hy_b), summed over the batch in
 // registers; Ghat (+)= the sum: one read-modify-write of Ghat per batch instead of per frame
 template <int L>
-__global__ void __launch_bounds__(LineEng<L>::NT, 1)
+__global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
     k_ref_r3b(const float2 *__restrict__ V, float2 *__restrict__ Ghat, const float2 *__restrict__ Href, int nb,
               const float4 *__restrict__ tw, const float2 *__restrict__ tw3, int N, int first) {
   using E = LineEng<L>;
@@ -207,27 +207,34 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
   typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
   const int col = blockIdx.x * E::G + st.g;
   const int o = (L - N) / 2;
-  float2 acc[16];
+  float2 acc[E::HOLD_SMEM ? 1 : E::R];
+  float2 *hold = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sm4) + E::SMEM) + threadIdx.x;
 #pragma unroll
-  for (int r = 0; r < 16; r++) acc[r] = make_float2(0.f, 0.f);
+  for (int r = 0; r < E::R; r++) {
+    if constexpr (E::HOLD_SMEM) hold[r * E::NT] = make_float2(0.f, 0.f); else acc[r] = make_float2(0.f, 0.f);
+  }
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *vin = V + (size_t)b * N * L;
     const float2 *Hy = Href + (size_t)b * 2 * L + L;
-    float2 v[16];
+    float2 v[E::R];
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int row = E::isp(st, r) - o;
       v[r] = (row >= 0 && row < N) ? ldg2(vin + p2(row, col, N)) : make_float2(0.f, 0.f);
     }
     E::fwd(v, st, tw, tw3);
 #pragma unroll
-    for (int r = 0; r < 16; r++) acc[r] = cadd(acc[r], cmulc(v[r], ldg2(Hy + E::ifr(st, r))));
+    for (int r = 0; r < E::R; r++) {
+      const float2 a = cmulc(v[r], ldg2(Hy + E::ifr(st, r)));
+      if constexpr (E::HOLD_SMEM) hold[r * E::NT] = cadd(hold[r * E::NT], a); else acc[r] = cadd(acc[r], a);
+    }
   }
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
+  for (int r = 0; r < E::R; r++) {
+    const float2 a = E::HOLD_SMEM ? hold[r * E::NT] : acc[r];
     float2 *p = Ghat + p2(E::ifr(st, r), col, L);
-    *p = first ? acc[r] : cadd(*p, acc[r]);
+    *p = first ? a : cadd(*p, a);
   }
 }
 
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
 // FWD  : W row (P2, N rows) x Hx -> inverse along x -> crop -> w frame (row-major N x N)
 // INIT : (a - mean) row (partial = &mean, fp64), zero-padded -> forward along x -> x conj(Hx) -> V
 template <int L, int MODE>
-__global__ void __launch_bounds__(LineEng<L>::NT, 1)
+__global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
     k_ref_rows(const float2 *__restrict__ in, const float *__restrict__ sqrt_d, float2 *__restrict__ out,
                double *__restrict__ partial, const float2 *__restrict__ Hx, const float4 *__restrict__ tw,
                const float2 *__restrict__ tw3, int N, float scale, int accumulate, float tau = 1.f) {
@@ -257,24 +264,24 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     if (partial) partial += MODE == REF_INIT ? fb : fb * gridDim.x;
     Hx += fb * 2 * L;
   }
-  float2 v[16];
+  float2 v[E::R];
   if (MODE == REF_QHAT) {
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = ldg2(in + (size_t)y * L + E::isp(st, r));
+    for (int r = 0; r < E::R; r++) v[r] = ldg2(in + (size_t)y * L + E::isp(st, r));
     E::fwd(v, st, tw, tw3);
 #pragma unroll
-    for (int r = 0; r < 16; r++) out[p2(y, E::ifr(st, r), L)] = v[r];
+    for (int r = 0; r < E::R; r++) out[p2(y, E::ifr(st, r), L)] = v[r];
   } else if (MODE == REF_R2) {
     const bool act = y < N;
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int f = E::ifr(st, r);
       v[r] = act ? cmul(ldg2(in + p2(y, f, N)), ldg2(Hx + f)) : make_float2(0.f, 0.f);
     }
     E::inv(v, st, tw, tw3);
     double acc = 0.0;
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int c = E::isp(st, r) - o;
       float2 w = make_float2(0.f, 0.f);
       if (act && c >= 0 && c < N) {
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     E::fwd(v, st, tw, tw3);
     if (act) {
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
+      for (int r = 0; r < E::R; r++) {
         const int f = E::ifr(st, r);
         out[p2(y, f, N)] = cmulc(v[r], ldg2(Hx + f));
       }
@@ -298,14 +305,14 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
     const bool act = y < N;
     const float c = (float)partial[0];
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int cc = E::isp(st, r) - o;
       v[r] = make_float2((act && cc >= 0 && cc < N) ? __ldg(sqrt_d + (size_t)y * N + cc) - c : 0.f, 0.f);
     }
     E::fwd(v, st, tw, tw3);
     if (act) {
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
+      for (int r = 0; r < E::R; r++) {
         const int f = E::ifr(st, r);
         out[p2(y, f, N)] = cmulc(v[r], ldg2(Hx + f));
       }
@@ -313,24 +320,24 @@ __global__ void __launch_bounds__(LineEng<L>::NT, 1)
   } else if (MODE == REF_FWD) {
     const bool act = y < N;
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       const int f = E::ifr(st, r);
       v[r] = act ? cmul(ldg2(in + p2(y, f, N)), ldg2(Hx + f)) : make_float2(0.f, 0.f);
     }
     E::inv(v, st, tw, tw3);
     if (act) {
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
+      for (int r = 0; r < E::R; r++) {
         const int c = E::isp(st, r) - o;
         if (c >= 0 && c < N) out[(size_t)y * N + c] = v[r];
       }
     }
   } else {  // FINAL
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = in[p2(y, E::ifr(st, r), L)];
+    for (int r = 0; r < E::R; r++) v[r] = in[p2(y, E::ifr(st, r), L)];
     E::inv(v, st, tw, tw3);
 #pragma unroll
-    for (int r = 0; r < 16; r++) {
+    for (int r = 0; r < E::R; r++) {
       float2 *p = out + (size_t)y * L + E::isp(st, r);
       const float2 a = cscale(v[r], scale);
       *p = accumulate ? cadd(*p, a) : a;

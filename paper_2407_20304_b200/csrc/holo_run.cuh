@@ -62,8 +62,9 @@ void set_ref_attrs() {
   a((const void *)k_ref_rows<L, REF_FINAL>);
   a((const void *)k_ref_rows<L, REF_FWD>);
   a((const void *)k_ref_rows<L, REF_INIT>);
-  a((const void *)k_ref_r1b<L>);
-  a((const void *)k_ref_r3b<L>);
+  const int sza = (int)LineEng<L>::SMEM_ACC;
+  cudaFuncSetAttribute((const void *)k_ref_r1b<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, sza);
+  cudaFuncSetAttribute((const void *)k_ref_r3b<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, sza);
 }
 
 template <int L>
@@ -397,7 +398,7 @@ struct RefRun {
       const int nb = R - r0 < p->BR ? R - r0 : p->BR;
       const float2 *H = p->Href + (size_t)r0 * 2 * L;
       pbeg(p);
-      k_ref_r1b<L><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, p->tw3, N);
+      k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, p->tw3, N);
       k_ref_rows<L, REF_FWD><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, nullptr, w + (size_t)r0 * N * N, nullptr, H,
                                                                        tw, p->tw3, N, 1.f, 0);
       pend(p, HOLO_PASS_REF, A + nb * (A + 8.0 * N * N), nb * fl * (L + N), 2);
@@ -421,7 +422,7 @@ struct RefRun {
       pbeg(p);
       k_ref_rows<L, REF_INIT><<<dim3(gn, nb), E::NT, SM, p->stream>>>(nullptr, sqrt_dref + r0 * NN, p->Vr,
                                                                         p->partR + r0, H, tw, p->tw3, N, 1.f, 0);
-      k_ref_r3b<L><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, p->tw3, N, r0 == 0);
+      k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, p->tw3, N, r0 == 0);
       pend(p, HOLO_PASS_REF, nb * A * (0.0625 + 0.5 + 0.5) + A * (r0 ? 2.0 : 1.0), nb * fl * (N + L), 2);
     }
     pbeg(p);
@@ -458,11 +459,11 @@ struct RefRun {
       const float2 *H = p->Href + (size_t)r0 * 2 * L;
       const bool f0 = first && r0 == 0;
       pbeg(p);
-      k_ref_r1b<L><<<gl, E::NT, SM, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, tw3, N);
+      k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, tw3, N);
       k_ref_rows<L, REF_R2><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
                                                                       p->partR + (size_t)r0 * gn, H, tw, tw3, N, 1.f,
                                                                       0, p->tau);
-      if (want_q) k_ref_r3b<L><<<gl, E::NT, SM, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, tw3, N, f0);
+      if (want_q) k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, tw3, N, f0);
       // bytes: Qhat once, W write + read, sqrt_d, V write + read per frame, Ghat once per batch
       pend(p, HOLO_PASS_REF,
            A + nb * A * (0.5 + 0.5 + 1.0 / 8 + 0.5 + (want_q ? 0.5 : 0.0)) + (want_q ? A * (f0 ? 1.0 : 2.0) : 0.0),
