@@ -45,6 +45,9 @@ struct holo_plan {
   std::vector<double> ref_shifts;
   // reference arm (holo_ref.cuh): Qhat, Ghat (P2, L x L), Wr, Vr (P2, N x L), Href [R][2][L], F partials
   float2 *Qhat = nullptr, *Ghat = nullptr, *Wr = nullptr, *Vr = nullptr, *Href = nullptr, *tw3 = nullptr;
+  // factored frame tables of the sweep passes (holo_ref.cuh R1B / R2 / R3B): hz [L] = h_{zeta0} / L and
+  // Hfac [R][2][FS] = per frame and axis the shift ramp as A[ref_R] (per engine value) x B[ref_T] (per thread)
+  float2 *hz = nullptr, *Hfac = nullptr;
   double *partR = nullptr;
   int ref_cap = 0;  // frames Href / partR are sized for
   int BR = 1;       // reference frames per batched launch (Wr / Vr hold BR frames)
@@ -99,6 +102,7 @@ struct HoloOps {
   void (*init_psi)(holo_plan *p, const float *sqrt_d, const float *sqrt_dref, double db, float2 *psi0);  // O18
   void (*init_probe)(holo_plan *p, const float *sqrt_dref, float2 *q0);                               // O17
   int ref_lines_per_cta;  // rows per CTA of the reference-arm row kernels (partials per frame)
+  int ref_R, ref_T;       // values per thread / threads per line of the reference-arm line engine
 };
 
 const HoloOps *holo_ops_for(int L);  // NULL if L is not built

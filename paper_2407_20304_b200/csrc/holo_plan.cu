@@ -434,9 +434,12 @@ holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
     const int nbr = (N + G - 1) / G;  // CTAs of one frame's R2 row pass (one F partial each)
     HC(cudaStreamSynchronize(p->stream));  // a queued reference sweep may still read them
     dfree(p, (void **)&p->Href);
+    dfree(p, (void **)&p->Hfac);
     dfree(p, (void **)&p->partR);
     p->ref_cap = 0;
     st = dalloc(p, &p->Href, sizeof(float2) * 2 * L * (size_t)n_ref);
+    if (st == HOLO_OK)
+      st = dalloc(p, &p->Hfac, sizeof(float2) * 2 * (size_t)(p->ops->ref_R + p->ops->ref_T) * n_ref);
     if (st == HOLO_OK) st = dalloc(p, &p->partR, sizeof(double) * (size_t)nbr * n_ref);
     if (st != HOLO_OK) return st;
     p->ref_cap = n_ref;
@@ -453,6 +456,39 @@ holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
       }
     }
   if (n_ref > 0) HC(cudaMemcpy(p->Href, H.data(), H.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  // factored form for the sweep passes: hz[f] = h_{zeta0}[f] / L, and per frame / axis the ramp
+  // r_s[f] = A[i] B[t] over the engine layout f = t + base(i) (t < ref_T: thread, i < ref_R: value):
+  // A[i] = e^{-2 pi i fbar(base(i)) s / L} (fbar's Nyquist wrap depends on i only: base(i) is a multiple
+  // of ref_T and so is L/2), B[t] = e^{-2 pi i t s / L}.  holo_ref.cuh LineEng<L>::ifr defines base(i).
+  if (!p->hz) {
+    st = dalloc(p, &p->hz, sizeof(float2) * L);
+    if (st != HOLO_OK) return st;
+    std::vector<float2> hzv(L);
+    for (int f = 0; f < L; f++) {
+      const cd v = h[f] / (double)L;
+      hzv[f] = make_float2((float)v.real(), (float)v.imag());
+    }
+    HC(cudaMemcpy(p->hz, hzv.data(), hzv.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
+  {
+    const int RE = p->ops->ref_R, TE = p->ops->ref_T, FS = RE + TE;
+    auto base = [&](int i) { return RE == 48 ? TE * (i % 16) + (L / 3) * (i / 16) : TE * i; };
+    std::vector<float2> Fv((size_t)2 * FS * n_ref);
+    for (int r = 0; r < n_ref; r++)
+      for (int ax = 0; ax < 2; ax++) {
+        const double sv = s[2 * r + ax];
+        float2 *o = Fv.data() + ((size_t)r * 2 + ax) * FS;
+        for (int i = 0; i < RE; i++) {
+          const cd v = expi2pi_frac(-(double)fbar(base(i), L) * sv / (double)L);
+          o[i] = make_float2((float)v.real(), (float)v.imag());
+        }
+        for (int t = 0; t < TE; t++) {
+          const cd v = expi2pi_frac(-(double)t * sv / (double)L);
+          o[RE + t] = make_float2((float)v.real(), (float)v.imag());
+        }
+      }
+    if (n_ref > 0) HC(cudaMemcpy(p->Hfac, Fv.data(), Fv.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
   p->n_ref = n_ref;
   p->ref_shifts.assign(s, s + 2 * n_ref);
   return HOLO_OK;

@@ -27,6 +27,7 @@ struct LineEng {  // power of two: the Stockham engine, G lines per 512-thread C
   using C = Cta<L, 512>;
   static constexpr int NT = 512, G = C::G, T = L / 16, R = 16, MINB = 1, MINB_ACC = 1;
   static constexpr bool HOLD_SMEM = false;  // R1B / R3B keep their second line in registers
+  static constexpr int FS = R + T;          // ramp factors per frame and axis (A[R], B[T])
   static constexpr size_t SMEM = C::XBYTES, SMEM_ACC = SMEM;
   struct St {
     Xch x;
@@ -62,6 +63,7 @@ struct LineEng<6144> {
   // R1B / R3B: the second line (Qhat column / batch sum) in a thread-private shared-memory slot
   // behind the exchange buffers (value i of thread t at SMEM + 8 (i NT + t): conflict free)
   static constexpr bool HOLD_SMEM = true;
+  static constexpr int FS = R + T;  // ramp factors per frame and axis (A[R], B[T])
   static constexpr size_t SMEM_ACC = SMEM + sizeof(float2) * (size_t)R * NT;
   struct St {
     float2 *buf;
@@ -163,11 +165,16 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
 
 // ---------------------------------------------------------------- batched column passes
 // B_r reference frames per launch; frame b's tables at Href + 2 L b (x row, then y row).
-// R1B: the Qhat column is read ONCE; per frame: x Hy_b, inverse along y, rows [o, o+N) -> W_b
+// The frame tables factor as H_b[f] = h[f] / L x r_{s_b}[f] (hz = h_{zeta0} / L, common to all frames)
+// and the ramp as r_s[f] = A[i] B[t] over the engine layout f = ifr(t, i) (fac: per frame and axis
+// FS = R + T values, ref_factors on the host), so a frame costs one table value per thread plus
+// R warp-uniform (L1 broadcast) values instead of a length-L table.
+// R1B: the Qhat column x hz is read ONCE; per frame: x ramp_b, inverse along y, rows [o, o+N) -> W_b
 template <int L>
 __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
-    k_ref_r1b(const float2 *__restrict__ Qhat, float2 *__restrict__ W, const float2 *__restrict__ Href, int nb,
-              const float4 *__restrict__ tw, const float2 *__restrict__ tw3, int N) {
+    k_ref_r1b(const float2 *__restrict__ Qhat, float2 *__restrict__ W, const float2 *__restrict__ hz,
+              const float2 *__restrict__ fac, int nb, const float4 *__restrict__ tw, const float2 *__restrict__ tw3,
+              int N) {
   using E = LineEng<L>;
   extern __shared__ float4 sm4[];
   typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
@@ -176,16 +183,18 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
   float2 q0[E::HOLD_SMEM ? 1 : E::R];
   float2 *hold = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sm4) + E::SMEM) + threadIdx.x;
 #pragma unroll
-  for (int r = 0; r < E::R; r++) {
-    const float2 a = ldg2(Qhat + p2(E::ifr(st, r), col, L));
+  for (int r = 0; r < E::R; r++) {  // the frame-independent part Qhat h_{zeta0} / L of the column
+    const int f = E::ifr(st, r);
+    const float2 a = cmul(ldg2(Qhat + p2(f, col, L)), ldg2(hz + f));
     if constexpr (E::HOLD_SMEM) hold[r * E::NT] = a; else q0[r] = a;
   }
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
-    const float2 *Hy = Href + (size_t)b * 2 * L + L;
+    const float2 *A = fac + (size_t)(2 * b + 1) * E::FS;  // y-axis ramp factors of frame b
+    const float2 Bt = ldg2(A + E::R + st.t);
     float2 v[E::R];
 #pragma unroll
-    for (int r = 0; r < E::R; r++) v[r] = cmul(E::HOLD_SMEM ? hold[r * E::NT] : q0[r], ldg2(Hy + E::ifr(st, r)));
+    for (int r = 0; r < E::R; r++) v[r] = cmul(E::HOLD_SMEM ? hold[r * E::NT] : q0[r], cmul(ldg2(A + r), Bt));
     E::inv(v, st, tw, tw3);
     float2 *w = W + (size_t)b * N * L;
 #pragma unroll
@@ -196,12 +205,13 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
   }
 }
 
-// R3B: per frame: pad(V_b col) -> forward along y -> x conj(Hy_b), summed over the batch in
-// registers; Ghat (+)= the sum: one read-modify-write of Ghat per batch instead of per frame
+// R3B: per frame: pad(V_b col) -> forward along y -> x conj(ramp_b), summed over the batch (registers
+// or the private smem slot), x conj(hz); Ghat (+)= the sum: one read-modify-write of Ghat per batch
 template <int L>
 __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
-    k_ref_r3b(const float2 *__restrict__ V, float2 *__restrict__ Ghat, const float2 *__restrict__ Href, int nb,
-              const float4 *__restrict__ tw, const float2 *__restrict__ tw3, int N, int first) {
+    k_ref_r3b(const float2 *__restrict__ V, float2 *__restrict__ Ghat, const float2 *__restrict__ hz,
+              const float2 *__restrict__ fac, int nb, const float4 *__restrict__ tw, const float2 *__restrict__ tw3,
+              int N, int first) {
   using E = LineEng<L>;
   extern __shared__ float4 sm4[];
   typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
@@ -216,7 +226,8 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *vin = V + (size_t)b * N * L;
-    const float2 *Hy = Href + (size_t)b * 2 * L + L;
+    const float2 *A = fac + (size_t)(2 * b + 1) * E::FS;
+    const float2 Bt = ldg2(A + E::R + st.t);
     float2 v[E::R];
 #pragma unroll
     for (int r = 0; r < E::R; r++) {
@@ -226,14 +237,15 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
     E::fwd(v, st, tw, tw3);
 #pragma unroll
     for (int r = 0; r < E::R; r++) {
-      const float2 a = cmulc(v[r], ldg2(Hy + E::ifr(st, r)));
+      const float2 a = cmulc(v[r], cmul(ldg2(A + r), Bt));  // x conj(ramp_b); conj(h)/L after the sum
       if constexpr (E::HOLD_SMEM) hold[r * E::NT] = cadd(hold[r * E::NT], a); else acc[r] = cadd(acc[r], a);
     }
   }
 #pragma unroll
   for (int r = 0; r < E::R; r++) {
-    const float2 a = E::HOLD_SMEM ? hold[r * E::NT] : acc[r];
-    float2 *p = Ghat + p2(E::ifr(st, r), col, L);
+    const int f = E::ifr(st, r);
+    const float2 a = cmulc(E::HOLD_SMEM ? hold[r * E::NT] : acc[r], ldg2(hz + f));
+    float2 *p = Ghat + p2(f, col, L);
     *p = first ? a : cadd(*p, a);
   }
 }
@@ -262,7 +274,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
     sqrt_d += fb * N * N;
     out += fb * (MODE == REF_FWD ? (size_t)N * N : (size_t)N * L);
     if (partial) partial += MODE == REF_INIT ? fb : fb * gridDim.x;
-    Hx += fb * 2 * L;
+    if (Hx) Hx += fb * 2 * L;
   }
   float2 v[E::R];
   if (MODE == REF_QHAT) {
@@ -271,7 +283,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
     E::fwd(v, st, tw, tw3);
 #pragma unroll
     for (int r = 0; r < E::R; r++) out[p2(y, E::ifr(st, r), L)] = v[r];
-  } else if (MODE == REF_R2) {
+  } else if (MODE == REF_R2) {  // the full frame table H_x (one frame per blockIdx.y: L2 / L1 resident)
     const bool act = y < N;
 #pragma unroll
     for (int r = 0; r < E::R; r++) {

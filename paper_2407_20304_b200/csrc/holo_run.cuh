@@ -397,8 +397,9 @@ struct RefRun {
     for (int r0 = 0; r0 < R; r0 += p->BR) {
       const int nb = R - r0 < p->BR ? R - r0 : p->BR;
       const float2 *H = p->Href + (size_t)r0 * 2 * L;
+      const float2 *F = p->Hfac + (size_t)r0 * 2 * E::FS;
       pbeg(p);
-      k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, p->tw3, N);
+      k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, p->tw3, N);
       k_ref_rows<L, REF_FWD><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, nullptr, w + (size_t)r0 * N * N, nullptr, H,
                                                                        tw, p->tw3, N, 1.f, 0);
       pend(p, HOLO_PASS_REF, A + nb * (A + 8.0 * N * N), nb * fl * (L + N), 2);
@@ -419,10 +420,11 @@ struct RefRun {
     for (int r0 = 0; r0 < R; r0 += p->BR) {
       const int nb = R - r0 < p->BR ? R - r0 : p->BR;
       const float2 *H = p->Href + (size_t)r0 * 2 * L;
+      const float2 *F = p->Hfac + (size_t)r0 * 2 * E::FS;
       pbeg(p);
       k_ref_rows<L, REF_INIT><<<dim3(gn, nb), E::NT, SM, p->stream>>>(nullptr, sqrt_dref + r0 * NN, p->Vr,
                                                                         p->partR + r0, H, tw, p->tw3, N, 1.f, 0);
-      k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, p->tw3, N, r0 == 0);
+      k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, p->hz, F, nb, tw, p->tw3, N, r0 == 0);
       pend(p, HOLO_PASS_REF, nb * A * (0.0625 + 0.5 + 0.5) + A * (r0 ? 2.0 : 1.0), nb * fl * (N + L), 2);
     }
     pbeg(p);
@@ -457,13 +459,14 @@ struct RefRun {
     for (int r0 = 0; r0 < R; r0 += p->BR) {
       const int nb = R - r0 < p->BR ? R - r0 : p->BR;
       const float2 *H = p->Href + (size_t)r0 * 2 * L;
+      const float2 *F = p->Hfac + (size_t)r0 * 2 * E::FS;
       const bool f0 = first && r0 == 0;
       pbeg(p);
-      k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, H, nb, tw, tw3, N);
+      k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, tw3, N);
       k_ref_rows<L, REF_R2><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
                                                                       p->partR + (size_t)r0 * gn, H, tw, tw3, N, 1.f,
                                                                       0, p->tau);
-      if (want_q) k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, H, nb, tw, tw3, N, f0);
+      if (want_q) k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, p->hz, F, nb, tw, tw3, N, f0);
       // bytes: Qhat once, W write + read, sqrt_d, V write + read per frame, Ghat once per batch
       pend(p, HOLO_PASS_REF,
            A + nb * A * (0.5 + 0.5 + 1.0 / 8 + 0.5 + (want_q ? 0.5 : 0.0)) + (want_q ? A * (f0 ? 1.0 : 2.0) : 0.0),
@@ -517,9 +520,10 @@ struct RefRun {
                                         holo_run::Run<LV>::upsample2,                                          \
                                         holo_run::Run<LV>::init_psi,                                           \
                                         holo_run::RefRun<LV>::init_probe,                                      \
-                                        holo::LineEng<LV>::G};
+                                        holo::LineEng<LV>::G, holo::LineEng<LV>::R, holo::LineEng<LV>::T};
 #define HOLO_DEFINE_REF_OPS(LV)                                                                                  \
   static void holo_set_attrs_##LV() { holo_run::set_ref_attrs<LV>(); }                                          \
   extern const HoloOps holo_ops_##LV = {LV,      holo_set_attrs_##LV,       nullptr, holo_run::RefRun<LV>::run, \
                                         holo_run::RefRun<LV>::fwd, nullptr, nullptr,                           \
-                                        holo_run::RefRun<LV>::init_probe, holo::LineEng<LV>::G};
+                                        holo_run::RefRun<LV>::init_probe, holo::LineEng<LV>::G,                \
+                                        holo::LineEng<LV>::R, holo::LineEng<LV>::T};
