@@ -415,6 +415,10 @@ __device__ __noinline__ TabPipe<L> x3_plane(const float2 *__restrict__ T3j, floa
     // parked in registers (as in X1)
 #pragma unroll
     for (int r = 0; r < 16; r++) Z[r] = ldg2(T3j + p2(y, t + r * T, L));
+    if (!last && (threadIdx.x & 3) == 0) {  // the next plane's rows into L2 (one lane per 32-byte sector)
+#pragma unroll
+      for (int r = 0; r < 16; r++) prefetch_l2_sector(T3j + (size_t)L * L + p2(y, t + r * T, L));
+    }
     float2 e[16];
     mag_adj<L>(
         v, [&](int r) { return Z[r]; }, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe,
@@ -457,6 +461,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   pipe.start(seq, slot_base<L, true>(sm), bars);
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 *grow = g + (size_t)y * L;  // also the Fourier-domain accumulator of sum_j W_j
+  if (eta && threadIdx.x == 0) prefetch_l2(eta + (size_t)blockIdx.x * C::G * L, 8u * C::G * L);  // read at the end
 #pragma unroll 1
   for (int j = 0; j < nz; j++)
     pipe = x3_plane<L>(T3 + (size_t)j * L * L, grow, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j, j + 1 == nz);

@@ -53,10 +53,13 @@ struct LineEng {  // power of two: the Stockham engine, G lines per 512-thread C
 // all three) and the radix-3 combine X[k + 2048 m] = sum_s W_3^{s m} W_6144^{s k} Y_s[k] is done in
 // registers (no third exchange).  Several CTAs per SM, so one CTA's exchange overlaps another's
 // butterflies.
+#ifndef HOLO_REF_MINB
+#define HOLO_REF_MINB 3
+#endif
 template <>
 struct LineEng<6144> {
   static constexpr int L = 6144, LS = 2048, NT = 128, G = 1, T = 128, R = 48;
-  static constexpr int MINB = 3;      // CTAs per SM of the plain passes (<= 170 registers)
+  static constexpr int MINB = HOLO_REF_MINB;  // CTAs per SM of the plain passes (3: <= 170 registers)
   static constexpr int MINB_ACC = 2;  // R1B / R3B keep a second 48-value line (Qhat column / Ghat sum)
   static constexpr int BS = Shape<LS>::LP;  // one sub-line's exchange buffer (float2)
   static constexpr size_t SMEM = sizeof(float2) * (size_t)BS * 3;
