@@ -253,6 +253,66 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
   }
 }
 
+#ifndef HOLO_R2B_PF_W
+#define HOLO_R2B_PF_W 0
+#endif
+// R2B (LineEng<6144>): row y of ALL nb frames of a batch in one CTA (the frame loop inside, as
+// R1B / R3B): the code stays hot in the instruction cache, and the next frame's W row and data row
+// are prefetched into L2 (one lane per 32-byte sector) while the current frame is transformed.
+// Per frame as REF_R2: W row x Hx_b, inverse along x, crop, residual (+F), pad, forward along x,
+// x conj(Hx_b) -> V_b; partial[fb * gridDim.x + y] = F of (frame fb, row y).
+template <int L>
+__global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
+    k_ref_r2b(const float2 *__restrict__ W, const float *__restrict__ sqrt_d, float2 *__restrict__ V,
+              double *__restrict__ partial, const float2 *__restrict__ H, const float4 *__restrict__ tw,
+              const float2 *__restrict__ tw3, int N, int nb, float tau) {
+  using E = LineEng<L>;
+  extern __shared__ float4 sm4[];
+  __shared__ double red[32];
+  typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
+  const int y = blockIdx.x;  // E::G == 1
+  const int o = (L - N) / 2;
+#pragma unroll 1
+  for (int fb = 0; fb < nb; fb++) {
+    const float2 *win = W + (size_t)fb * N * L;
+    const float2 *Hx = H + (size_t)fb * 2 * L;
+    const float *drow = sqrt_d + (size_t)fb * N * N + (size_t)y * N;
+    float2 v[E::R];
+#pragma unroll
+    for (int r = 0; r < E::R; r++) {
+      const int f = E::ifr(st, r);
+      v[r] = cmul(ldg2(win + p2(y, f, N)), ldg2(Hx + f));
+    }
+    if (fb + 1 < nb) {  // the next frame's data row into L2 (its W row: R2B_PF_W)
+#if HOLO_R2B_PF_W
+      if ((threadIdx.x & 1) == 0) {
+#pragma unroll
+        for (int r = 0; r < E::R; r++) prefetch_l2_sector(win + (size_t)N * L + p2(y, E::ifr(st, r), N));
+      }
+#endif
+      for (int i = threadIdx.x; i < (N * 4 + 31) / 32; i += E::NT) prefetch_l2_sector(drow + (size_t)N * N + 8 * i);
+    }
+    E::inv(v, st, tw, tw3);
+    double acc = 0.0;
+#pragma unroll
+    for (int r = 0; r < E::R; r++) {
+      const int c = E::isp(st, r) - o;
+      float2 w = make_float2(0.f, 0.f);
+      if (c >= 0 && c < N) w = residual_tau(v[r], __ldg(drow + c), tau, acc);  // G_tau, App. A.3
+      v[r] = w;
+    }
+    const double sum = block_sum(acc, red);
+    if (threadIdx.x == 0) partial[(size_t)fb * gridDim.x + y] = sum;
+    E::fwd(v, st, tw, tw3);
+    float2 *vo = V + (size_t)fb * N * L;
+#pragma unroll
+    for (int r = 0; r < E::R; r++) {
+      const int f = E::ifr(st, r);
+      vo[p2(y, f, N)] = cmulc(v[r], ldg2(Hx + f));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- row passes
 // QHAT : q row (row-major) -> forward along x -> Qx (P2)
 // R2   : W row (P2, N rows) x Hx -> inverse along x -> crop, residual (+F), pad ->

@@ -62,6 +62,7 @@ void set_ref_attrs() {
   a((const void *)k_ref_rows<L, REF_FINAL>);
   a((const void *)k_ref_rows<L, REF_FWD>);
   a((const void *)k_ref_rows<L, REF_INIT>);
+  a((const void *)k_ref_r2b<L>);
   const int sza = (int)LineEng<L>::SMEM_ACC;
   cudaFuncSetAttribute((const void *)k_ref_r1b<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, sza);
   cudaFuncSetAttribute((const void *)k_ref_r3b<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, sza);
@@ -463,9 +464,14 @@ struct RefRun {
       const bool f0 = first && r0 == 0;
       pbeg(p);
       k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, tw3, N);
-      k_ref_rows<L, REF_R2><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
-                                                                      p->partR + (size_t)r0 * gn, H, tw, tw3, N, 1.f,
-                                                                      0, p->tau);
+      if constexpr (E::HOLD_SMEM) {  // LineEng<6144>: one row of every frame of the batch per CTA (gn == N)
+        k_ref_r2b<L><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
+                                                    p->partR + (size_t)r0 * gn, H, tw, tw3, N, nb, p->tau);
+      } else {
+        k_ref_rows<L, REF_R2><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
+                                                                        p->partR + (size_t)r0 * gn, H, tw, tw3, N, 1.f,
+                                                                        0, p->tau);
+      }
       if (want_q) k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, p->hz, F, nb, tw, tw3, N, f0);
       // bytes: Qhat once, W write + read, sqrt_d, V write + read per frame, Ghat once per batch
       pend(p, HOLO_PASS_REF,
