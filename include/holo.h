@@ -225,6 +225,22 @@ holo_status holo_bin2(holo_plan *p, const float *fine, float *coarse, int32_t co
 holo_status holo_init_probe(holo_plan *p, const float *sqrt_dref, void *q0);
 holo_status holo_init_psi(holo_plan *p, const float *sqrt_d, const float *sqrt_dref, double delta_beta, void *psi0);
 
+/* Fourier-domain object state (Parseval; SURVEY 8(e) "run CG ... in the Fourier domain").
+ * holo_set_fourier(p, 1): every later holo_fwd / holo_adj / holo_grad / holo_grad_full call on this
+ * plan takes psi and eta_psi_prev, and returns grad_psi / adj_psi, as the 2-D DFTs of the object-domain
+ * arrays (psi~_k = DFT2(psi_k), unnormalised: psi~[fy][fx] = sum_{y,x} psi[y][x] e^{-2 pi i (fy y + fx x)/npad},
+ * row-major, natural frequency order), while F, sc[1] = ||grad_psi||^2 and sc[2] = Re<grad_psi, eta_psi_prev>
+ * stay the object-domain values (Parseval: the transformed dots / npad^2).  The operators are unchanged;
+ * the chain skips the transforms that only move the object in and out of the Fourier domain (X1's row
+ * FFT, Y1's column FFT, Y2's column IFFT and X3's row IFFT: 2.5 of ~21.5 line transforms per frame).
+ * The CG step is pointwise and linear, so it runs unchanged on the transformed arrays.  Default 0.
+ * HOLO_EUNSUPPORTED for npad 6144.
+ * holo_fourier: out[m] = DFT2(in[m]) (inverse = 0) or IDFT2(in[m]) = (1/npad^2) sum e^{+...} (inverse = 1)
+ * for m < count, row-major [count][npad][npad] complex64; in == out allowed (the plan's scratch sits
+ * between the two passes).  Not usable while a sweep of the same plan is pending on another stream. */
+holo_status holo_set_fourier(holo_plan *p, int32_t on);
+holo_status holo_fourier(holo_plan *p, const void *in, void *out, int32_t count, int32_t inverse);
+
 /* Number of kernel launches this plan has enqueued since creation (profiling aid). */
 uint64_t holo_launch_count(const holo_plan *p);
 

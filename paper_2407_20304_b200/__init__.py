@@ -101,6 +101,10 @@ _lib.holo_set_gq_event.argtypes = [_P, _P]
 _lib.holo_set_gq_event.restype = _S
 _lib.holo_set_tau.argtypes = [_P, ctypes.c_double]
 _lib.holo_set_tau.restype = _S
+_lib.holo_set_fourier.argtypes = [_P, ctypes.c_int32]
+_lib.holo_set_fourier.restype = _S
+_lib.holo_fourier.argtypes = [_P, _P, _P, ctypes.c_int32, ctypes.c_int32]
+_lib.holo_fourier.restype = _S
 
 _lib.holo_profile_enable.argtypes = [_P, ctypes.c_int]
 _lib.holo_profile_enable.restype = _S
@@ -116,7 +120,7 @@ EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes"
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
             "holo_grad_ref", "holo_fwd_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
             "holo_profile_read", "holo_upsample2", "holo_bin2", "holo_init_probe", "holo_init_psi",
-            "holo_set_probe_shifts", "holo_grad_full", "holo_set_gq_event", "holo_set_tau"]
+            "holo_set_probe_shifts", "holo_grad_full", "holo_set_gq_event", "holo_set_tau", "holo_set_fourier", "holo_fourier"]
 
 
 class HoloError(RuntimeError):
@@ -146,6 +150,7 @@ class Plan:
 
     def __init__(self, n, npad, z1, n_angles, wavelength, focus_to_detector, detector_pixel, device=0,
                  stream=None, angle_batch=None):
+        self.fourier_state = False  # holo_set_fourier
         if angle_batch is None:  # default: 8 angles per Y1/X2/Y2 launch
             angle_batch = max(1, min(8, n_angles))
         g = HoloGeometry()
@@ -226,6 +231,20 @@ class Plan:
     def set_tau(self, tau):
         """holo_set_tau: penalty exponent of G_tau (App. A.3) for later grad calls (1 = F_1, 2 = F_2)."""
         self._chk(_lib.holo_set_tau(self._h, float(tau)))
+
+    def set_fourier(self, on):
+        """holo_set_fourier: object-side arrays of later fwd / adj / grad calls are DFT2(psi) (unnormalised)."""
+        self._chk(_lib.holo_set_fourier(self._h, int(bool(on))))
+        self.fourier_state = bool(on)
+
+    def fourier(self, x, out=None, inverse=False):
+        """holo_fourier: out[m] = DFT2(x[m]) (numpy.fft.fft2) or, inverse, IDFT2 (numpy.fft.ifft2); x [M][npad][npad]."""
+        LL = self.npad ** 2
+        M = x.numel() // LL
+        out = x if out is None else out
+        self._chk(_lib.holo_fourier(self._h, _ptr(x, torch.complex64, M * LL, "x"), _ptr(out, torch.complex64, M * LL, "out"),
+                                    M, int(bool(inverse))))
+        return out
 
     def set_probe_shifts(self, s):
         """holo_set_probe_shifts: per-frame probe shifts s^p [K][nz][2] (None: plain q_j path)."""

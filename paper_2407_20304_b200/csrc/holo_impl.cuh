@@ -59,6 +59,7 @@ struct holo_plan {
   // per-frame probe shifts (O19, holo_set_probe_shifts): Hq [K][nz][2][L] = h_omega_j r_{s^p_kj} / L per axis;
   // Qt [B][nz][L][L] (IDFT_x(Hq_x Qhat), P2), Qk [B][L][L] (q_kj, P2), Ut [B][nz][L][L] (probe-gradient terms)
   bool ps = false;
+  bool fourier = false;  // holo_set_fourier: the object-side arrays are DFT2(psi) (Fourier-domain CG state)
   cudaEvent_t gq_event = nullptr;  // holo_set_gq_event: recorded when grad_q_part is complete
   float2 *hq = nullptr, *Qt = nullptr, *Qk = nullptr, *Ut = nullptr;
   // per-pass event profiling (holo_profile_*)
@@ -103,6 +104,7 @@ struct HoloOps {
   void (*init_probe)(holo_plan *p, const float *sqrt_dref, float2 *q0);                               // O17
   int ref_lines_per_cta;  // rows per CTA of the reference-arm row kernels (partials per frame)
   int ref_R, ref_T;       // values per thread / threads per line of the reference-arm line engine
+  void (*dft2)(holo_plan *p, const float2 *in, float2 *out, int count, int inverse);  // holo_fourier; NULL: 6144
 };
 
 const HoloOps *holo_ops_for(int L);  // NULL if L is not built

@@ -88,7 +88,7 @@ __device__ __noinline__ TabPipe<L> x1_plane(float2 *__restrict__ T1j, const floa
 template <int L>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1, Tables tb, const __grid_constant__ TabSeq seq,
-         int nz, uint32_t magmask) {
+         int nz, uint32_t magmask, int fourier) {
   using C = CtaK<L>;
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     const int t = C::t(), y = blockIdx.x * C::G + C::g();
     float2 v[16];
     ld_row<L>(v, psi_k + (size_t)y * L, t);
-    fft<L, false>(v, x, t, tb.tw);
+    if (!fourier) fft<L, false>(v, x, t, tb.tw);  // HOLO_FOURIER: the row of DFT2(psi) IS the x-spectrum
 #pragma unroll
     for (int r = 0; r < 16; r++) X[r] = v[r];
   }
@@ -125,7 +125,7 @@ template <int L, bool PS>
 __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const float2 *__restrict__ qj,
                                       const float2 *__restrict__ qt, float2 *__restrict__ qk,
                                       float2 *__restrict__ aout, float2 *__restrict__ w1, const float4 *__restrict__ tw,
-                                      const TabSeq &seq, TabPipe<L> pipe, float2 *sm, int mag, int N) {
+                                      const TabSeq &seq, TabPipe<L> pipe, float2 *sm, int mag, int N, int fourier) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   Xch x = C::xch(sm);
@@ -133,7 +133,7 @@ __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
   float2 v[16];
   ld_p2_col<L>(v, in, col, L, t);
-  fft<L, false>(v, x, t, tw);
+  if (!fourier) fft<L, false>(v, x, t, tw);  // HOLO_FOURIER: T1 is already the y-spectrum (X1 ran on DFT2 psi)
   if (mag) {
 #pragma unroll
     for (int r = 0; r < 16; r++) X[r] = v[r];
@@ -187,7 +187,7 @@ template <int L, bool PS>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_y1(const float2 *__restrict__ T1j, size_t fstride, const float2 *__restrict__ qj, const float2 *__restrict__ Qt,
          float2 *__restrict__ Qk, float2 *__restrict__ Aout, float2 *__restrict__ W1, Tables tb,
-         const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
+         const __grid_constant__ TabSeq seq, int mag, int N, int nb, int fourier) {
   using C = CtaK<L>;
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     if (threadIdx.x == 0 && b + 1 < nb) prefetch_l2(in + fstride + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
     pipe = y1_frame<L, PS>(in, qj, PS ? Qt + (size_t)b * fstride : nullptr, (PS && Qk) ? Qk + (size_t)b * L * L : nullptr,
                     Aout ? Aout + (size_t)b * L * L : nullptr, W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq, pipe,
-                    sm, mag, N);
+                    sm, mag, N, fourier);
   }
 }
 
@@ -305,7 +305,7 @@ template <int L, bool PS>
 __device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, const float2 *__restrict__ ab,
                                       const float2 *__restrict__ qj, float2 *__restrict__ Gj, float2 *__restrict__ ut,
                                       float2 *__restrict__ t3, const float4 *__restrict__ tw, const TabSeq &seq,
-                                      TabPipe<L> pipe, float2 *sm, int mag, int N) {
+                                      TabPipe<L> pipe, float2 *sm, int mag, int N, int fourier) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   Xch x = C::xch(sm);
@@ -363,7 +363,7 @@ __device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, cons
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
     pipe.done(seq);
   }
-  fft<L, true>(v, x, t, tw);
+  if (!fourier) fft<L, true>(v, x, t, tw);  // HOLO_FOURIER: T3 keeps the y-spectrum (X3 works on it row by row)
   st_p2_col<L>(v, t3, col, L, t);
   return pipe;
 }
@@ -372,7 +372,7 @@ template <int L, bool PS>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_y2(const float2 *__restrict__ V1, const float2 *__restrict__ a, const float2 *__restrict__ qj,
          const float2 *__restrict__ Qk, float2 *__restrict__ Gj, float2 *__restrict__ Ut, float2 *__restrict__ T3j,
-         size_t fstride, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N, int nb) {
+         size_t fstride, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N, int nb, int fourier) {
   using C = CtaK<L>;
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       if (wq) prefetch_l2(ab + (size_t)L * L + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
     }
     pipe = y2_frame<L, PS>(vin, ab, PS ? Qk + (size_t)b * L * L : qj, Gj, (PS && Ut) ? Ut + (size_t)b * fstride : nullptr,
-                    T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N);
+                    T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N, fourier);
   }
 }
 
@@ -450,7 +450,7 @@ template <int L>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x3(const float2 *__restrict__ T3, const float2 *__restrict__ eta, float2 *__restrict__ g,
          double *__restrict__ partial, Tables tb, const __grid_constant__ TabSeq seq, int nz, uint32_t magmask,
-         float scale) {
+         float scale, int fourier) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   extern __shared__ float4 sm4[];
@@ -470,7 +470,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = Z[r];
-  fft<L, true>(v, x, t, tb.tw);
+  // HOLO_FOURIER: the rows are y-spectral (T3 from Y2) and the x-spectrum is kept: g = DFT2(grad) / L^2
+  // before the caller's scale (2 L^2), and the dots carry Parseval's 1/L^2
+  if (!fourier) fft<L, true>(v, x, t, tb.tw);
   double gg = 0.0, ge = 0.0;
 #pragma unroll
   for (int r = 0; r < 16; r++) {
@@ -485,8 +487,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   const double s0 = block_sum(gg, red);
   const double s1 = block_sum(ge, red);
   if (threadIdx.x == 0) {
-    partial[2 * blockIdx.x] = s0;
-    partial[2 * blockIdx.x + 1] = s1;
+    const double ps = fourier ? 1.0 / ((double)L * L) : 1.0;  // Parseval: object-domain dots
+    partial[2 * blockIdx.x] = s0 * ps;
+    partial[2 * blockIdx.x + 1] = s1 * ps;
   }
 }
 
@@ -620,6 +623,36 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 }
 
 // layout conversion (plane without propagation, omega_j = 0):  P2 <-> row-major, out (+)= scale * in
+// ------------------------------------------------------------------ Fourier-domain object state
+// holo_fourier: out = DFT2(in) (unnormalised, numpy.fft.fft2 convention) or IDFT2(in) (numpy.fft.ifft2,
+// 1 / L^2), row-major L x L: a row pass into a P2 scratch, then a column pass writing row-major.
+template <int L, bool INV>
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
+    k_dft2_rows(const float2 *__restrict__ in, float2 *__restrict__ out, const float4 *__restrict__ tw) {
+  using C = CtaK<L>;
+  extern __shared__ float4 sm4[];
+  Xch x = C::xch(reinterpret_cast<float2 *>(sm4));
+  const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  float2 v[16];
+  ld_row<L>(v, in + (size_t)y * L, t);
+  fft<L, INV>(v, x, t, tw);
+  st_p2_row<L>(v, out, y, L, t);
+}
+template <int L, bool INV>
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
+    k_dft2_cols(const float2 *__restrict__ in, float2 *__restrict__ out, const float4 *__restrict__ tw, float scale) {
+  using C = CtaK<L>;
+  extern __shared__ float4 sm4[];
+  Xch x = C::xch(reinterpret_cast<float2 *>(sm4));
+  const int t = C::t(), col = blockIdx.x * C::G + C::g();
+  float2 v[16];
+  ld_p2_col<L>(v, in, col, L, t);
+  fft<L, INV>(v, x, t, tw);
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = cscale(v[r], scale);
+  st_col<L>(v, out + col, t);
+}
+
 static __global__ void k_p2_convert(const float2 *__restrict__ in, float2 *__restrict__ out, int L, int to_p2, float scale,
                              int accumulate) {
   const size_t n = (size_t)L * L;

@@ -676,6 +676,24 @@ holo_status holo_upsample2(holo_plan *p, const void *coarse, void *fine, int32_t
   return postcheck(p);
 }
 
+holo_status holo_set_fourier(holo_plan *p, int32_t on) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (on && !p->ops->dft2) return fail(p, HOLO_EUNSUPPORTED, "the Fourier-domain object state needs a power-of-two npad");
+  p->fourier = on != 0;
+  return HOLO_OK;
+}
+
+holo_status holo_fourier(holo_plan *p, const void *in, void *out, int32_t count, int32_t inverse) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (count < 0 || (count > 0 && (!in || !out))) return fail(p, HOLO_EINVAL, "bad holo_fourier arguments");
+  if (!p->ops->dft2) return fail(p, HOLO_EUNSUPPORTED, "holo_fourier needs a power-of-two npad");
+  if (count == 0) return HOLO_OK;
+  p->ops->dft2(p, (const float2 *)in, (float2 *)out, count, inverse != 0);
+  return postcheck(p);
+}
+
 holo_status holo_bin2(holo_plan *p, const float *fine, float *coarse, int32_t count) {
   holo_status st = precheck(p);
   if (st != HOLO_OK) return st;

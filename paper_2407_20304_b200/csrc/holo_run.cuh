@@ -27,6 +27,10 @@ void set_chain_attrs() {
   using S = Smem<L>;
   auto a = [](const void *f, size_t s) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s); };
   a((const void *)k_x1<L>, S::XPT);
+  a((const void *)k_dft2_rows<L, false>, S::X);
+  a((const void *)k_dft2_rows<L, true>, S::X);
+  a((const void *)k_dft2_cols<L, false>, S::X);
+  a((const void *)k_dft2_cols<L, true>, S::X);
   a((const void *)k_y1<L, false>, S::XPT);
   a((const void *)k_y1<L, true>, S::XPT);
   a((const void *)k_xq<L>, S::XPT);
@@ -128,6 +132,23 @@ struct Run {
     }
   }
 
+  // holo_fourier: out[m] = DFT2(in[m]) or IDFT2(in[m]) (row-major), via the T1 workspace (P2)
+  static void dft2(holo_plan *p, const float2 *in, float2 *out, int count, int inverse) {
+    const float4 *tw = reinterpret_cast<const float4 *>(p->tw);
+    const size_t LL = (size_t)L * L;
+    for (int m = 0; m < count; m++) {
+      pbeg(p);
+      if (inverse) {
+        k_dft2_rows<L, true><<<L / G, NT, SM::X, p->stream>>>(in + m * LL, p->T1, tw);
+        k_dft2_cols<L, true><<<L / G, NT, SM::X, p->stream>>>(p->T1, out + m * LL, tw, 1.0f / ((float)L * L));
+      } else {
+        k_dft2_rows<L, false><<<L / G, NT, SM::X, p->stream>>>(in + m * LL, p->T1, tw);
+        k_dft2_cols<L, false><<<L / G, NT, SM::X, p->stream>>>(p->T1, out + m * LL, tw, 1.0f);
+      }
+      pend(p, HOLO_PASS_FILTER, 4 * A, 2.0 * L * fftf(L), 2);
+    }
+  }
+
   // O18: multi-distance Paganin initial object of every angle (holo_init.cuh)
   static void init_psi(holo_plan *p, const float *sqrt_d, const float *sqrt_dref, double db, float2 *psi0) {
     const Tables tb = p->tables();
@@ -197,6 +218,7 @@ struct Run {
     const int nbx2 = p->nbx2;
     const double fl = fftf(L), rN = (double)N / L, NN8 = 8.0 * N * N;
     const bool gq_pass = want_q && (mode == 0 || mode == 2);
+    const int fo_ = p->fourier ? 1 : 0;  // holo_set_fourier: psi / eta / grad_psi are DFT2 of the object arrays
     int nmag = 0;
     for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
     if (ps) {
@@ -234,8 +256,8 @@ struct Run {
           }
           pbeg(p);
           k_x1<L><<<L / G, NT, SM::XPT, p->stream>>>(psi + (size_t)k * LL, p->T1 + (size_t)b * nz * LL, tb, q, nz,
-                                                      p->magmask);
-          pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * (1 + 4 * nmag + (nz - nmag)));
+                                                      p->magmask, fo_);
+          pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * ((fo_ ? 0 : 1) + 4 * nmag + (nz - nmag)));
           if (ps) {
             TabSeq qq{};
             for (int j = 0; j < nz; j++) qq.p[qq.n++] = hqp(k, j, 0);
@@ -265,14 +287,14 @@ struct Run {
           if (ps)
             k_y1<L, true><<<L / G, NT, SM::XPT, p->stream>>>(p->T1 + (size_t)j * LL, (size_t)nz * LL, nullptr,
                                                               p->Qt + (size_t)j * LL, p->Qk, aout, w1, tb, q, mag, N,
-                                                              nb);
+                                                              nb, fo_);
           else
             k_y1<L, false><<<L / G, NT, SM::XPT, p->stream>>>(p->T1 + (size_t)j * LL, (size_t)nz * LL, qjj, nullptr,
-                                                               nullptr, aout, w1, tb, q, mag, N, nb);
+                                                               nullptr, aout, w1, tb, q, mag, N, nb, fo_);
           // bytes: T1 read, Aw write, W1 write per frame; q_j once per batch (L2-resident); PS: Qt read, Qk write
           pend(p, HOLO_PASS_Y1,
                nb * (A + (w1 ? rN * A : 0) + (aout ? A : 0) + (ps ? 2 * A : 0)) + ((w1 && !ps) ? A : 0),
-               nb * L * fl * (1 + (mag ? 4 : 1) + (w1 ? 2 : 0) + (ps ? 1 : 0)));
+               nb * L * fl * ((fo_ ? 0 : 1) + (mag ? 4 : 1) + (w1 ? 2 : 0) + (ps ? 1 : 0)));
         }
         // ---- X2 (batched over blockIdx.y)
         double *pf = p->partF + ((size_t)k0 * nz + j) * nbx2;
@@ -322,16 +344,16 @@ struct Run {
         pbeg(p);
         if (ps)
           k_y2<L, true><<<L / G, NT, SM::XPT, p->stream>>>(p->V1, p->Aw, nullptr, p->Qk, nullptr, Utj, T3j,
-                                                            (size_t)nz * LL, tb, q2, mag, N, nb);
+                                                            (size_t)nz * LL, tb, q2, mag, N, nb, fo_);
         else
           k_y2<L, false><<<L / G, NT, SM::XPT, p->stream>>>(p->V1, p->Aw, qjj, nullptr, Gj, nullptr, T3j,
-                                                             (size_t)nz * LL, tb, q2, mag, N, nb);
+                                                             (size_t)nz * LL, tb, q2, mag, N, nb, fo_);
         // bytes: V1 read, Aw read (q gradient), T3 write per frame; G_j read + write and q_j once per batch
         // (PS: Qk read per frame, Ut write per frame)
         pend(p, HOLO_PASS_Y2,
              nb * (rN * A + (want_q ? A : 0) + (T3j ? A : 0) + (ps ? ((T3j ? A : 0) + (want_q ? A : 0)) : 0)) +
                  (Gj ? 2 * A : 0) + ((T3j && !ps) ? A : 0),
-             nb * L * fl * (2 + (T3j ? (mag ? 5 : 2) : 0) + (Utj ? 1 : 0)));
+             nb * L * fl * (2 + (T3j ? (mag ? 5 : 2) - (fo_ ? 1 : 0) : 0) + (Utj ? 1 : 0)));
       }
       // ---- X3 (per angle): g_k = 2 IFFT_x( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3[b][j];
       //      PS: XG, Ghat (+)= sum_j conj(Hq_x) FFT_x(Ut[b][j]).
@@ -359,8 +381,8 @@ struct Run {
         pbeg(p);
         k_x3<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T3 + (size_t)b * nz * LL, eta ? eta + (size_t)k * LL : nullptr,
                                                     gpsi + (size_t)k * LL, p->partX3 + (size_t)k * 2 * p->nbx3, tb, q3,
-                                                    nz, p->magmask, gscale);
-        pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + 1));
+                                                    nz, p->magmask, fo_ ? gscale * (float)L * (float)L : gscale, fo_);
+        pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + (fo_ ? 0 : 1)));
       };
       const bool want_x3 = gpsi && (mode == 0 || mode == 2);
       if (!last_batch) {
@@ -526,10 +548,11 @@ struct RefRun {
                                         holo_run::Run<LV>::upsample2,                                          \
                                         holo_run::Run<LV>::init_psi,                                           \
                                         holo_run::RefRun<LV>::init_probe,                                      \
-                                        holo::LineEng<LV>::G, holo::LineEng<LV>::R, holo::LineEng<LV>::T};
+                                        holo::LineEng<LV>::G, holo::LineEng<LV>::R, holo::LineEng<LV>::T,      \
+                                        holo_run::Run<LV>::dft2};
 #define HOLO_DEFINE_REF_OPS(LV)                                                                                  \
   static void holo_set_attrs_##LV() { holo_run::set_ref_attrs<LV>(); }                                          \
   extern const HoloOps holo_ops_##LV = {LV,      holo_set_attrs_##LV,       nullptr, holo_run::RefRun<LV>::run, \
                                         holo_run::RefRun<LV>::fwd, nullptr, nullptr,                           \
                                         holo_run::RefRun<LV>::init_probe, holo::LineEng<LV>::G,                \
-                                        holo::LineEng<LV>::R, holo::LineEng<LV>::T};
+                                        holo::LineEng<LV>::R, holo::LineEng<LV>::T, nullptr};

@@ -27,7 +27,7 @@ class JointCG:
     a plan with n_angles = 0 then runs the probe-only problem of configs[4] (rho_psi unused)."""
 
     def __init__(self, plan, sqrt_d, psi0, q0, rho_psi=1.0, rho_q=1.0, gamma_init=1.0, max_halvings=12,
-                 group=None, distributed=None, sqrt_dref=None, fused=None, overlap=True):
+                 group=None, distributed=None, sqrt_dref=None, fused=None, overlap=True, fourier=None):
         self.plan = plan
         self.d = sqrt_d
         self.dref = sqrt_dref
@@ -43,11 +43,22 @@ class JointCG:
         self.dist = dist.is_available() and dist.is_initialized() if distributed is None else distributed
         dev = psi0.device
         z = lambda t: torch.zeros_like(t)
-        self.psi, self.q = psi0.contiguous().clone(), q0.contiguous().clone()
-        self.psi_t, self.q_t = z(self.psi), z(self.q)
-        self.eta_psi, self.eta_q = z(self.psi), z(self.q)
-        self.g_psi, self.g_q = z(self.psi), z(self.q)
-        self.gt_psi, self.gt_q = z(self.psi), z(self.q)
+        # Fourier-domain object state (holo_set_fourier, Parseval): the psi block (psi, eta, g, trial) is
+        # held as DFT2 of the object arrays, which saves the chain's four "into / out of the Fourier
+        # domain" transforms per sweep; the CG step is linear and the library returns object-domain dots,
+        # so the iteration is the same.  `psi` converts back on access.
+        if fourier is None:
+            fourier = hasattr(plan, "set_fourier") and psi0.numel() > 0 and psi0.is_cuda
+        self.fourier = bool(fourier)
+        if hasattr(plan, "set_fourier") and psi0.numel() > 0:
+            plan.set_fourier(self.fourier)
+        self._psi, self.q = psi0.contiguous().clone(), q0.contiguous().clone()
+        if self.fourier:
+            plan.fourier(self._psi)
+        self.psi_t, self.q_t = z(self._psi), z(self.q)
+        self.eta_psi, self.eta_q = z(self._psi), z(self.q)
+        self.g_psi, self.g_q = z(self._psi), z(self.q)
+        self.gt_psi, self.gt_q = z(self._psi), z(self.q)
         self.sc = torch.zeros(5, dtype=torch.float64, device=dev)
         # g_q / X3 overlap: only with CUDA tensors, an NCCL group and a plan exposing the hook
         self.comm = self.gq_ev = None
@@ -64,6 +75,13 @@ class JointCG:
         self.stagnated = True
         self.m = 0
         self.sweeps = 0
+
+    @property
+    def psi(self):
+        """The object block in the object domain (a converted copy in Fourier mode)."""
+        if not self.fourier:
+            return self._psi
+        return self.plan.fourier(self._psi, torch.empty_like(self._psi), inverse=True)
 
     # ------------------------------------------------------------------ sweep
     def sweep(self, psi, q, eta_psi, eta_q, g_psi, g_q):
@@ -109,7 +127,7 @@ class JointCG:
         return s
 
     def start(self):
-        s = self.sweep(self.psi, self.q, None, None, self.g_psi, self.g_q)
+        s = self.sweep(self._psi, self.q, None, None, self.g_psi, self.g_q)
         self.F = s[0]
         self.dots = s
         return self.F
@@ -128,7 +146,7 @@ class JointCG:
             gamma = float(forced_gamma)
         cin = HoloCgIn(self.gPg(), self.g_eta, self.gprev_eta, gamma, self.rho[0], self.rho[1], int(first), 0)
         qb = (None,) * 4 if self.q_frozen else (self.q, self.eta_q, self.g_q, self.q_t)
-        out = p.cg_step(cin, self.psi, self.eta_psi, self.g_psi, self.psi_t, *qb)
+        out = p.cg_step(cin, self._psi, self.eta_psi, self.g_psi, self.psi_t, *qb)
         g_eta_new = out.g_eta_new
         accepted = False
         tries = 0
@@ -143,9 +161,9 @@ class JointCG:
             gamma *= 0.5
             cin = HoloCgIn(0.0, 0.0, 0.0, gamma, self.rho[0], self.rho[1], 0, 1)
             qb = (None,) * 4 if self.q_frozen else (self.q, self.eta_q, None, self.q_t)
-            p.cg_step(cin, self.psi, self.eta_psi, None, self.psi_t, *qb)
+            p.cg_step(cin, self._psi, self.eta_psi, None, self.psi_t, *qb)
         if accepted:
-            self.psi, self.psi_t = self.psi_t, self.psi
+            self._psi, self.psi_t = self.psi_t, self._psi
             if not self.q_frozen:
                 self.q, self.q_t = self.q_t, self.q
             self.g_psi, self.gt_psi = self.gt_psi, self.g_psi

@@ -36,8 +36,10 @@ def host(t):
     return t.cpu().numpy().astype(np.complex128 if t.is_complex() else np.float64)
 
 
-@pytest.mark.parametrize("batch", [1, 4])
-def test_cg_two_iterations_cfg0_vs_oracle(batch):
+@pytest.mark.parametrize("batch,fourier", [(1, False), (4, False), (4, True)])
+def test_cg_two_iterations_cfg0_vs_oracle(batch, fourier):
+    """fourier: the psi block is held as DFT2 of the object arrays (holo_set_fourier); the oracle's
+    eta_psi is compared through numpy.fft.fft2, psi through JointCG.psi (converted back)."""
     import paper_2407_20304_b200 as hb
     from paper_2407_20304_b200.solver import JointCG
     cfg = synth.CONFIGS["cfg0"]
@@ -70,18 +72,20 @@ def test_cg_two_iterations_cfg0_vs_oracle(batch):
     plan = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=0, angle_batch=batch)
     plan.set_shifts(s)
     cg = JointCG(plan, dev(d, torch.float32), dev(x0[0]), dev(x0[1]), rho_psi=rho[0], rho_q=rho[1],
-                 distributed=False)
+                 distributed=False, fourier=fourier)
+    assert cg.fourier == fourier
+    Fd = (lambda a: np.fft.fft2(a, axes=(-2, -1))) if fourier else (lambda a: a)
     assert abs(cg.start() - F0) / F0 < TOL
     h1 = cg.iterate(forced_gamma=gam[0])
     assert abs(h1["F"] - F1) / F1 < TOL and h1["beta"] == 0.0 and h1["reset"]
-    assert rel(host(cg.eta_psi), eta0[0]) < TOL and rel(host(cg.eta_q), eta0[1]) < TOL
+    assert rel(host(cg.eta_psi), Fd(eta0[0])) < TOL and rel(host(cg.eta_q), eta0[1]) < TOL
     assert rel(host(cg.psi), x1[0]) < TOL and rel(host(cg.q), x1[1]) < TOL
     ge = ocg.rdot(g1, eta0)  # Re<g_1, eta_0> (psi + q blocks), from the fused sweep scalars
     assert abs(cg.g_eta - ge) / abs(ge) < TOL
     h2 = cg.iterate(forced_gamma=gam[1])
     assert abs(h2["beta"] - beta1) / abs(beta1) < TOL and not h2["reset"]
     assert abs(h2["F"] - F2) / F2 < TOL
-    assert rel(host(cg.eta_psi), eta1[0]) < TOL and rel(host(cg.eta_q), eta1[1]) < TOL
+    assert rel(host(cg.eta_psi), Fd(eta1[0])) < TOL and rel(host(cg.eta_q), eta1[1]) < TOL
     assert rel(host(cg.psi), x2[0]) < TOL and rel(host(cg.q), x2[1]) < TOL
     assert abs(cg.g_eta - ocg.rdot(g2, eta1)) / abs(ocg.rdot(g2, eta1)) < TOL
 

@@ -1,0 +1,126 @@
+"""Fourier-domain object state (holo_set_fourier / holo_fourier) against the oracle.
+
+With the flag set, holo_grad takes psi~ = DFT2(psi) (and eta~) and returns grad~ = DFT2(grad_psi),
+while F and the dots stay the object-domain values (Parseval).  The expected values are the
+oracle's object-domain results passed through numpy.fft.fft2 (a library transform of the
+oracle's output, never a GPU value).  Tolerances as the object-domain parity tests:
+2e-5 forward, 1e-4 gradients / F / dots.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import np_oracle as npo
+
+pytestmark = pytest.mark.gpu
+
+F2 = lambda a: np.fft.fft2(a, axes=(-2, -1))
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm((a - b).ravel()) / np.linalg.norm(b.ravel()))
+
+
+def dev(x, dt=torch.complex64):
+    return torch.as_tensor(np.ascontiguousarray(x)).to(dt).cuda().contiguous()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().astype(np.complex128 if t.is_complex() else np.float64)
+
+
+def plan(cfg, K, L=None, N=None, batch=None):
+    import paper_2407_20304_b200 as hb
+    return hb.Plan(cfg.n if N is None else N, cfg.npad if L is None else L, cfg.z1, K, cfg.wavelength, cfg.Z,
+                   cfg.det_pixel, device=0, angle_batch=batch)
+
+
+@pytest.mark.parametrize("L", [128, 512, 4096])
+def test_holo_fourier_matches_numpy(L):
+    cfg = synth.CONFIGS["cfg1"]
+    rng = np.random.default_rng(L)
+    M = 2 if L < 4096 else 1
+    x = rng.standard_normal((M, L, L)) + 1j * rng.standard_normal((M, L, L))
+    p = plan(cfg, 1, L=L, N=L // 2)
+    y = torch.empty(M, L, L, dtype=torch.complex64, device="cuda")
+    p.fourier(dev(x), y)
+    assert rel(host(y), F2(x)) < 2e-6
+    z = p.fourier(y.clone(), inverse=True)  # in place
+    assert rel(host(z), x) < 2e-6
+
+
+def _case(name, K):
+    cfg = synth.CONFIGS[name]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    psi_t = synth.psi_stack(cfg, K=K).numpy()
+    q_t = synth.probe(cfg).numpy()
+    s = synth.shifts(cfg, K=K)
+    return cfg, g, psi_t, q_t, s
+
+
+@pytest.mark.parametrize("name,K,batch", [("cfg0", 4, 4), ("cfg0", 3, 2), ("cfg1", 2, 2)])
+def test_grad_fourier_mode_parity(name, K, batch):
+    """holo_grad in Fourier mode: F, grad~ = fft2(grad_psi), grad_q, ||g||^2, Re<g, eta> vs the oracle;
+    also holo_fwd (w from psi~) and holo_adj (adj~ = fft2 of the object-domain adjoint)."""
+    cfg, g, psi_t, q_t, s = _case(name, K)
+    L, N = cfg.npad, cfg.n
+    pr = npo.Problem(g, L, N)
+    out = pr.fwd(psi_t, q_t, s)
+    w_t = np.stack([np.stack([out[(k, j)] for j in range(cfg.nz)]) for k in range(K)])
+    d = synth.poisson_amplitude(np.abs(w_t) ** 2, cfg.photons, cfg)
+    psi = np.exp(0.2j * np.random.default_rng(5).standard_normal(psi_t.shape)) * psi_t
+    q = 0.9 * q_t
+    F, gp, gq = pr.grad(psi, q, s, d)
+    eta = -gp * (1 + 0.1 * np.random.default_rng(6).standard_normal(gp.shape))
+    p = plan(cfg, K, batch=batch)
+    p.set_shifts(s)
+    p.set_fourier(True)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(q.shape, dtype=torch.complex64, device="cuda")
+    p.grad(dev(F2(psi)), dev(q), dev(d, torch.float32), sc, dev(F2(eta)), gpsi, gqd)
+    scs = host(sc).real
+    assert abs(scs[0] - F) / F < 1e-4
+    assert rel(host(gpsi), F2(gp)) < 1e-4 and rel(host(gqd), gq) < 1e-4
+    assert abs(scs[1] - np.vdot(gp, gp).real) / np.vdot(gp, gp).real < 1e-4
+    ge = np.vdot(eta, gp).real
+    assert abs(scs[2] - ge) / abs(ge) < 1e-4
+    # forward and adjoint with psi~
+    w = torch.empty(K, cfg.nz, N, N, dtype=torch.complex64, device="cuda")
+    p.fwd(dev(F2(psi)), dev(q), w)
+    wo = pr.fwd(psi, q, s)
+    for k in range(K):
+        for j in range(cfg.nz):
+            assert rel(host(w)[k, j], wo[(k, j)]) < 2e-5
+    y = np.random.default_rng(7).standard_normal((K, cfg.nz, N, N)) * (1 + 1j)
+    ad = torch.empty(psi.shape, dtype=torch.complex64, device="cuda")
+    p.adj(dev(y), dev(F2(psi)), dev(q), ad, None)
+    p.set_fourier(False)
+    ad0 = torch.empty(psi.shape, dtype=torch.complex64, device="cuda")
+    p.adj(dev(y), dev(psi), dev(q), ad0, None)
+    assert rel(host(ad), F2(host(ad0))) < 1e-5
+
+
+def test_grad_fourier_mode_full_size_one_angle():
+    """cfg3 (4096^2 torus), one angle, all four planes: Fourier mode vs the numpy oracle."""
+    cfg, g, psi_t, q_t, s = _case("cfg3", 1)
+    L, N = cfg.npad, cfg.n
+    pr = npo.Problem(g, L, N)
+    out = pr.fwd(psi_t, q_t, s)
+    d = np.stack([np.stack([np.abs(out[(0, j)]) for j in range(cfg.nz)])])
+    psi = np.ones_like(psi_t)
+    q = 0.9 * q_t
+    F, gp, gq = pr.grad(psi, q, s, d)
+    p = plan(cfg, 1, batch=1)
+    p.set_shifts(s)
+    p.set_fourier(True)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(q.shape, dtype=torch.complex64, device="cuda")
+    p.grad(dev(F2(psi)), dev(q), dev(d, torch.float32), sc, None, gpsi, gqd)
+    assert abs(host(sc).real[0] - F) / F < 1e-4
+    assert rel(host(gpsi), F2(gp)) < 1e-4 and rel(host(gqd), gq) < 1e-4
