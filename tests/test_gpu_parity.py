@@ -152,8 +152,10 @@ def test_cfg0_adjoint_parity(cfg0):
     assert rel(host(gap), ap) < TOL_G and rel(host(gaq), aq) < TOL_G
 
 
-def test_cfg1_parity_two_angles():
-    c = Case("cfg1", 2, oracle_kind="np")
+@pytest.mark.parametrize("K", [2, 8])
+def test_cfg1_parity_two_angles(K):
+    """cfg1 (512^2 torus, 4 planes); K = 8 is SURVEY 8(c)'s "8 angles x 4 distances" (one batch of 8)."""
+    c = Case("cfg1", K, oracle_kind="np")
     p = make_plan(c.cfg, c.K)
     p.set_shifts(c.s)
     w = torch.empty(c.K, c.cfg.nz, c.cfg.n, c.cfg.n, dtype=torch.complex64, device="cuda")
