@@ -177,7 +177,8 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 // Table slots: 2 (default; table i + 1 streams into the other slot while table i is in use)
 // or 1 (HOLO_TAB_SLOTS=1, for two CTAs per SM: the slot is refilled by done() right after
-// each use, so the load overlaps the transform that follows).
+// each use, so the load overlaps the transform that follows), or 0 (no slots: the steps read
+// the tables from global memory at their use, L2 / L1 resident).
 #ifndef HOLO_TAB_SLOTS
 #define HOLO_TAB_SLOTS 2
 #endif
@@ -190,6 +191,7 @@ struct TabPipe {
   static constexpr size_t BYTES = SLOTS * sizeof(float2) * L;
 
   __device__ __forceinline__ void issue(const TabSeq &q, int i) {
+    if constexpr (SLOTS == 0) return;
     if (threadIdx.x == 0 && i < q.n) {
       fence_proxy_async();  // earlier generic reads of this slot precede the async write
       mbar_expect_tx(bar + (i & (SLOTS - 1)), L * sizeof(float2));
@@ -201,6 +203,7 @@ struct TabPipe {
     slot = sm_slots;
     bar = bars;
     used = 0;
+    if constexpr (SLOTS == 0) return;  // tables read from global memory (L2 / L1) at their use
     if (threadIdx.x == 0) {
       for (int b = 0; b < SLOTS; b++) mbar_init(bar + b, 1);
       fence_mbar_init();
@@ -214,7 +217,9 @@ struct TabPipe {
   // (done() refilled it).
   __device__ __forceinline__ const float2 *take(const TabSeq &q, bool sync = false) {
     const int i = used++;
-    if constexpr (SLOTS == 2) {
+    if constexpr (SLOTS == 0) {
+      return q.p[i];
+    } else if constexpr (SLOTS == 2) {
       if (i >= 1) {
         // the slot being refilled held table i - 1: every LINE must be done with it.  The
         // transforms' barriers guarantee that only within a line when lines sync
