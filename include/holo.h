@@ -225,6 +225,14 @@ holo_status holo_bin2(holo_plan *p, const float *fine, float *coarse, int32_t co
 holo_status holo_init_probe(holo_plan *p, const float *sqrt_dref, void *q0);
 holo_status holo_init_psi(holo_plan *p, const float *sqrt_d, const float *sqrt_dref, double delta_beta, void *psi0);
 
+/* Staged data (end-to-end streaming): the next holo_grad / holo_grad_full call whose sqrt_d argument
+ * is dev_sqrt_d first copies host_sqrt_d (PINNED host memory, [K][nz][n][n] float32) into it, one angle
+ * batch at a time on a plan-owned copy stream that starts after everything already queued on the
+ * plan's stream; each batch's residual pass waits only for its own slice, so the transfer of batch
+ * b + 1 overlaps the passes of batch b.  Later calls read the resident data.  NULL pointers cancel a
+ * pending stage.  The host buffer must stay valid until that call's work has completed. */
+holo_status holo_stage_sqrt_d(holo_plan *p, const float *host_sqrt_d, float *dev_sqrt_d);
+
 /* Fourier-domain object state (Parseval; SURVEY 8(e) "run CG ... in the Fourier domain").
  * holo_set_fourier(p, 1): every later holo_fwd / holo_adj / holo_grad / holo_grad_full call on this
  * plan takes psi and eta_psi_prev, and returns grad_psi / adj_psi, as the 2-D DFTs of the object-domain

@@ -60,6 +60,13 @@ struct holo_plan {
   // Qt [B][nz][L][L] (IDFT_x(Hq_x Qhat), P2), Qk [B][L][L] (q_kj, P2), Ut [B][nz][L][L] (probe-gradient terms)
   bool ps = false;
   bool fourier = false;  // holo_set_fourier: the object-side arrays are DFT2(psi) (Fourier-domain CG state)
+  // holo_stage_sqrt_d: a pending host -> device copy of the data, streamed per angle batch on a copy
+  // stream by the next sweep that reads stage_dev (each batch's X2 waits for its own event)
+  const float *stage_host = nullptr;
+  float *stage_dev = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t stage_start = nullptr;
+  std::vector<cudaEvent_t> stage_ev;
   cudaEvent_t gq_event = nullptr;  // holo_set_gq_event: recorded when grad_q_part is complete
   float2 *hq = nullptr, *Qt = nullptr, *Qk = nullptr, *Ut = nullptr;
   // per-pass event profiling (holo_profile_*)

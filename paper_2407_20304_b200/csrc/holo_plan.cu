@@ -350,6 +350,9 @@ void holo_plan_destroy(holo_plan *p) {
   if (!p) return;
   cudaSetDevice(p->device);
   for (cudaEvent_t e : p->evpool) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->stage_ev) cudaEventDestroy(e);
+  if (p->stage_start) cudaEventDestroy(p->stage_start);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   for (void *a : p->allocs) cudaFree(a);
   delete p;
 }
@@ -674,6 +677,27 @@ holo_status holo_upsample2(holo_plan *p, const void *coarse, void *fine, int32_t
   if (count == 0) return HOLO_OK;
   p->ops->upsample2(p, (const float2 *)coarse, (float2 *)fine, count);
   return postcheck(p);
+}
+
+holo_status holo_stage_sqrt_d(holo_plan *p, const float *host_sqrt_d, float *dev_sqrt_d) {
+  holo_status st = precheck(p);
+  if (st != HOLO_OK) return st;
+  if (!host_sqrt_d || !dev_sqrt_d) {  // cancel
+    p->stage_host = nullptr;
+    p->stage_dev = nullptr;
+    return HOLO_OK;
+  }
+  if (p->K == 0) return HOLO_OK;
+  if (!p->copy_stream) {
+    HC(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    HC(cudaEventCreateWithFlags(&p->stage_start, cudaEventDisableTiming));
+    const int nbatch = (p->K + p->B - 1) / p->B;
+    p->stage_ev.resize(nbatch);
+    for (auto &e : p->stage_ev) HC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  p->stage_host = host_sqrt_d;
+  p->stage_dev = dev_sqrt_d;
+  return HOLO_OK;
 }
 
 holo_status holo_set_fourier(holo_plan *p, int32_t on) {

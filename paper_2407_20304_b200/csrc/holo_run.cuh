@@ -241,6 +241,23 @@ struct Run {
       for (auto *e : list) q.p[q.n++] = e;
     };
     const bool need_fwd_chain = (mode != 2) || want_q || ps;
+    // holo_stage_sqrt_d: stream the data in per angle batch on the copy stream (after everything
+    // queued so far on the plan's stream, i.e. the previous readers of the device buffer), so batch
+    // b + 1's copy overlaps batch b's passes; batch b's first X2 waits for its own event
+    const bool staged = p->stage_dev && sqrt_d == p->stage_dev && (mode == 0 || mode == 3);
+    if (staged) {
+      cudaEventRecord(p->stage_start, p->stream);
+      cudaStreamWaitEvent(p->copy_stream, p->stage_start, 0);
+      for (int k0 = 0, bi = 0; k0 < K; k0 += p->B, bi++) {
+        const int nb = K - k0 < p->B ? K - k0 : p->B;
+        const size_t off = (size_t)k0 * nz * NN, cnt = (size_t)nb * nz * NN;
+        cudaMemcpyAsync(p->stage_dev + off, p->stage_host + off, cnt * sizeof(float), cudaMemcpyHostToDevice,
+                        p->copy_stream);
+        cudaEventRecord(p->stage_ev[bi], p->copy_stream);
+      }
+      p->stage_host = nullptr;
+      p->stage_dev = nullptr;
+    }
     for (int k0 = 0; k0 < K; k0 += p->B) {
       const int nb = K - k0 < p->B ? K - k0 : p->B;  // ragged last batch
       // ---- X1 (per angle): T1[b][j] = (M S)_x psi_k rows;  PS: XQ, Qt[b][j] = IFFT_x(Hq_x Qhat)
@@ -296,7 +313,8 @@ struct Run {
                nb * (A + (w1 ? rN * A : 0) + (aout ? A : 0) + (ps ? 2 * A : 0)) + ((w1 && !ps) ? A : 0),
                nb * L * fl * ((fo_ ? 0 : 1) + (mag ? 4 : 1) + (w1 ? 2 : 0) + (ps ? 1 : 0)));
         }
-        // ---- X2 (batched over blockIdx.y)
+        // ---- X2 (batched over blockIdx.y); a staged batch's data must have arrived (X1 / Y1 overlapped it)
+        if (staged && j == 0) cudaStreamWaitEvent(p->stream, p->stage_ev[k0 / p->B], 0);
         double *pf = p->partF + ((size_t)k0 * nz + j) * nbx2;
         TabSeq qh{};
         qh.p[qh.n++] = p->hdet + (size_t)j * L;
