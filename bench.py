@@ -545,10 +545,10 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         sw1 = solver.sweeps
         e0.record()
-        stage = cfg.name != "cfg4" and hasattr(plan, "stage_sqrt_d")
+        stage = hasattr(plan, "stage_sqrt_d")
         for _ in range(ns):
-            if stage:  # holo_stage_sqrt_d: streamed per angle batch inside the step's first sweep
-                plan.stage_sqrt_d(host_d, sqrt_d)
+            if stage:  # holo_stage_sqrt_d(ref): streamed per angle / frame batch inside the step's first sweep
+                (plan.stage_sqrt_dref if cfg.name == "cfg4" else plan.stage_sqrt_d)(host_d, sqrt_d)
             else:
                 sqrt_d.copy_(host_d, non_blocking=True)
             solver.iterate()  # ends with the D2H read of F and the dots
@@ -560,7 +560,7 @@ def main():
         e_sweeps = solver.sweeps - sw1
         e2e = {"value": frames * ns / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(sqrt_d.numel() * 4), "d2h_bytes_per_step": int(40 * e_sweeps / ns),
-               "steps": ns, "h2d": "holo_stage_sqrt_d: per angle batch on a copy stream, overlapped with the "
+               "steps": ns, "h2d": "holo_stage_sqrt_d(ref): per angle (reference-frame) batch on a copy stream, overlapped with the "
                                    "sweep" if stage else "one copy before the step"}
         del host_d
 

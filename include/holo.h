@@ -232,6 +232,9 @@ holo_status holo_init_psi(holo_plan *p, const float *sqrt_d, const float *sqrt_d
  * b + 1 overlaps the passes of batch b.  Later calls read the resident data.  NULL pointers cancel a
  * pending stage.  The host buffer must stay valid until that call's work has completed. */
 holo_status holo_stage_sqrt_d(holo_plan *p, const float *host_sqrt_d, float *dev_sqrt_d);
+/* The same for the reference frames (sqrt_dref [R][n][n] of holo_grad_ref / holo_grad_full): streamed per
+ * batch of reference frames, each batch's row pass (R2) waiting for its own slice. */
+holo_status holo_stage_sqrt_dref(holo_plan *p, const float *host_sqrt_dref, float *dev_sqrt_dref);
 
 /* Fourier-domain object state (Parseval; SURVEY 8(e) "run CG ... in the Fourier domain").
  * holo_set_fourier(p, 1): every later holo_fwd / holo_adj / holo_grad / holo_grad_full call on this

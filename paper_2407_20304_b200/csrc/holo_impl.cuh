@@ -64,6 +64,7 @@ struct holo_plan {
   // stream by the next sweep that reads stage_dev (each batch's X2 waits for its own event)
   const float *stage_host = nullptr;
   float *stage_dev = nullptr;
+  bool stage_ref = false;  // the staged array is the reference frames (holo_stage_sqrt_dref)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t stage_start = nullptr;
   std::vector<cudaEvent_t> stage_ev;

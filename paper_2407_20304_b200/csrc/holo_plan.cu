@@ -679,25 +679,37 @@ holo_status holo_upsample2(holo_plan *p, const void *coarse, void *fine, int32_t
   return postcheck(p);
 }
 
-holo_status holo_stage_sqrt_d(holo_plan *p, const float *host_sqrt_d, float *dev_sqrt_d) {
+namespace {
+holo_status stage_impl(holo_plan *p, const float *host, float *dev, bool ref) {
   holo_status st = precheck(p);
   if (st != HOLO_OK) return st;
-  if (!host_sqrt_d || !dev_sqrt_d) {  // cancel
-    p->stage_host = nullptr;
-    p->stage_dev = nullptr;
-    return HOLO_OK;
-  }
-  if (p->K == 0) return HOLO_OK;
+  p->stage_host = nullptr;
+  p->stage_dev = nullptr;
+  if (!host || !dev) return HOLO_OK;  // cancel
+  const int nbatch = ref ? (p->n_ref + p->BR - 1) / p->BR : (p->K + p->B - 1) / p->B;
+  if (nbatch == 0) return HOLO_OK;
   if (!p->copy_stream) {
     HC(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
     HC(cudaEventCreateWithFlags(&p->stage_start, cudaEventDisableTiming));
-    const int nbatch = (p->K + p->B - 1) / p->B;
-    p->stage_ev.resize(nbatch);
-    for (auto &e : p->stage_ev) HC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  p->stage_host = host_sqrt_d;
-  p->stage_dev = dev_sqrt_d;
+  while ((int)p->stage_ev.size() < nbatch) {
+    cudaEvent_t e;
+    HC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->stage_ev.push_back(e);
+  }
+  p->stage_host = host;
+  p->stage_dev = dev;
+  p->stage_ref = ref;
   return HOLO_OK;
+}
+}  // namespace
+
+holo_status holo_stage_sqrt_d(holo_plan *p, const float *host_sqrt_d, float *dev_sqrt_d) {
+  return stage_impl(p, host_sqrt_d, dev_sqrt_d, false);
+}
+
+holo_status holo_stage_sqrt_dref(holo_plan *p, const float *host_sqrt_dref, float *dev_sqrt_dref) {
+  return stage_impl(p, host_sqrt_dref, dev_sqrt_dref, true);
 }
 
 holo_status holo_set_fourier(holo_plan *p, int32_t on) {

@@ -244,7 +244,7 @@ struct Run {
     // holo_stage_sqrt_d: stream the data in per angle batch on the copy stream (after everything
     // queued so far on the plan's stream, i.e. the previous readers of the device buffer), so batch
     // b + 1's copy overlaps batch b's passes; batch b's first X2 waits for its own event
-    const bool staged = p->stage_dev && sqrt_d == p->stage_dev && (mode == 0 || mode == 3);
+    const bool staged = !p->stage_ref && p->stage_dev && sqrt_d == p->stage_dev && (mode == 0 || mode == 3);
     if (staged) {
       cudaEventRecord(p->stage_start, p->stream);
       cudaStreamWaitEvent(p->copy_stream, p->stage_start, 0);
@@ -496,6 +496,22 @@ struct RefRun {
     const float2 *tw3 = p->tw3;
     const int gl = L / E::G, gn = (N + E::G - 1) / E::G;
     const double A = 8.0 * L * L, fl = fftf(L);
+    // holo_stage_sqrt_d on the reference frames: streamed per frame batch on the copy stream, each
+    // batch's R2 waiting for its own slice (R1B of the batch overlaps it)
+    const size_t NNr = (size_t)N * N;
+    const bool staged = p->stage_ref && p->stage_dev && sqrt_dref == p->stage_dev;
+    if (staged) {
+      cudaEventRecord(p->stage_start, p->stream);
+      cudaStreamWaitEvent(p->copy_stream, p->stage_start, 0);
+      for (int r0 = 0, bi = 0; r0 < R; r0 += p->BR, bi++) {
+        const int nb = R - r0 < p->BR ? R - r0 : p->BR;
+        cudaMemcpyAsync(p->stage_dev + r0 * NNr, p->stage_host + r0 * NNr, nb * NNr * sizeof(float),
+                        cudaMemcpyHostToDevice, p->copy_stream);
+        cudaEventRecord(p->stage_ev[bi], p->copy_stream);
+      }
+      p->stage_host = nullptr;
+      p->stage_dev = nullptr;
+    }
     // B_r frames per launch: the Qhat column read once (R1B), Ghat read-modify-written once (R3B)
     for (int r0 = 0; r0 < R; r0 += p->BR) {
       const int nb = R - r0 < p->BR ? R - r0 : p->BR;
@@ -504,6 +520,7 @@ struct RefRun {
       const bool f0 = first && r0 == 0;
       pbeg(p);
       k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, tw3, N);
+      if (staged) cudaStreamWaitEvent(p->stream, p->stage_ev[r0 / p->BR], 0);
       if constexpr (E::HOLD_SMEM) {  // LineEng<6144>: one row of every frame of the batch per CTA (gn == N)
         k_ref_r2b<L><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
                                                     p->partR + (size_t)r0 * gn, H, tw, tw3, N, nb, p->tau);

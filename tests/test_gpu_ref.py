@@ -163,3 +163,28 @@ def test_ref_arm_g_tau_parity(tau):
     Fg, gg = run_gpu(p, q, d)
     assert abs(Fg - F) / F < TOL_S
     assert rel(gg, gq) < TOL_G
+
+
+def test_ref_arm_staged_data_matches_resident():
+    """holo_stage_sqrt_dref: reference frames streamed from pinned host memory per frame batch give
+    the same F and grad_q as device-resident frames, bit for bit (12 frames: batches of 8 + 4)."""
+    cfg = synth.CONFIGS["cfg4"]
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    L, N, R = 256, 128, 12
+    q_t = synth.probe(cfg, L=L).numpy()
+    rs = np.random.default_rng(29).uniform(-8, 8, size=(R, 2))
+    d = ref_data(g, q_t, rs, N, 29).astype(np.float32)
+    p = plan(cfg, L, N)
+    p.set_ref_shifts(rs)
+    res = []
+    for staged in (False, True):
+        dd = dev(d, torch.float32) if not staged else torch.zeros(d.shape, dtype=torch.float32, device="cuda")
+        if staged:
+            p.stage_sqrt_dref(torch.from_numpy(np.ascontiguousarray(d)).pin_memory(), dd)
+        sc = torch.zeros(1, dtype=torch.float64, device="cuda")
+        gq = torch.empty(L, L, dtype=torch.complex64, device="cuda")
+        p.grad_ref(dev(0.9 * q_t), dd, sc, gq)
+        torch.cuda.synchronize()
+        res.append((sc.cpu().numpy(), gq.cpu().numpy(), dd.cpu().numpy()))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[1][2], d)
