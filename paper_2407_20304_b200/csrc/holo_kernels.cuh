@@ -93,16 +93,20 @@ __device__ __forceinline__ void red_add2(float2 *p, float2 v) {
 // carries the remaining factor 2 in the gradient).  tau = 1 is F_1 (Eq. (10)): rho = w - a w/|w|;
 // tau = 2 is F_2 (Eq. (9)): rho = 2 (|w|^2 - a^2) w.  rho = 0 where w = 0 (reading C7, all tau).
 // tau is uniform over the launch, so the branches do not diverge.
+// TM: 0 = tau 1, 1 = tau 2, 2 = general tau, -1 = decided at run time.  The kernels on the hot path
+// are instantiated per TM so that only one branch is compiled into their (fully unrolled) loops:
+// three interleaved unrolled branches cost instruction-cache misses in the 6144-point R2B pass.
+template <int TM = -1>
 __device__ __forceinline__ float2 residual_tau(float2 w, float a, float tau, double &acc) {
   const float m2 = w.x * w.x + w.y * w.y;
-  if (tau == 1.0f) {
+  if (TM == 0 || (TM < 0 && tau == 1.0f)) {
     const float m = sqrtf(m2);
     const float dm = m - a;
     acc += (double)(dm * dm);
     const float f = m > 0.f ? 1.0f - __fdividef(a, m) : 0.f;
     return cscale(w, f);
   }
-  if (tau == 2.0f) {
+  if (TM == 1 || (TM < 0 && tau == 2.0f)) {
     const float dm = m2 - a * a;
     acc += (double)dm * (double)dm;
     return cscale(w, 2.0f * dm);

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 //   ADJ : y frame row (row-major) -> pad, D_x^* -> V1
 //   OBJ : W1 row -> D_x, crop, F only
 // Strides between the batch's frames: in / out (elements), sqrt_d (elements), partial (CTAs).
-template <int L, int MODE>
+template <int L, int MODE, int TM = -1>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x2(const float2 *__restrict__ in, size_t in_stride, const float *__restrict__ sqrt_d, size_t d_stride,
          float2 *__restrict__ out, size_t out_stride, double *__restrict__ partial, int part_stride, Tables tb,
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       const int c = t + r * T - o;
       float2 w = make_float2(0.f, 0.f);
       if (act && c >= 0 && c < N) {
-        w = residual_tau(v[r], dv[r], tau, acc);  // G_tau (App. A.3): F_1 at tau = 1, F_2 at 2
+        w = residual_tau<TM>(v[r], dv[r], tau, acc);  // G_tau (App. A.3): F_1 at tau = 1, F_2 at 2
       }
       v[r] = w;
     }

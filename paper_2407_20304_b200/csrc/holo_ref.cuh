@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
 // are prefetched into L2 (one lane per 32-byte sector) while the current frame is transformed.
 // Per frame as REF_R2: W row x Hx_b, inverse along x, crop, residual (+F), pad, forward along x,
 // x conj(Hx_b) -> V_b; partial[fb * gridDim.x + y] = F of (frame fb, row y).
-template <int L>
+template <int L, int TM = -1>
 __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
     k_ref_r2b(const float2 *__restrict__ W, const float *__restrict__ sqrt_d, float2 *__restrict__ V,
               double *__restrict__ partial, const float2 *__restrict__ H, const float4 *__restrict__ tw,
@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
     for (int r = 0; r < E::R; r++) {
       const int c = E::isp(st, r) - o;
       float2 w = make_float2(0.f, 0.f);
-      if (c >= 0 && c < N) w = residual_tau(v[r], __ldg(drow + c), tau, acc);  // G_tau, App. A.3
+      if (c >= 0 && c < N) w = residual_tau<TM>(v[r], __ldg(drow + c), tau, acc);  // G_tau, App. A.3
       v[r] = w;
     }
     const double sum = block_sum(acc, red);

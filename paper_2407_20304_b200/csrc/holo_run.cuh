@@ -35,10 +35,14 @@ void set_chain_attrs() {
   a((const void *)k_y1<L, true>, S::XPT);
   a((const void *)k_xq<L>, S::XPT);
   a((const void *)k_xg<L>, S::XPT);
-  a((const void *)k_x2<L, X2_GRAD>, S::XT);
+  a((const void *)k_x2<L, X2_GRAD, 0>, S::XT);
+  a((const void *)k_x2<L, X2_GRAD, 1>, S::XT);
+  a((const void *)k_x2<L, X2_GRAD, 2>, S::XT);
+  a((const void *)k_x2<L, X2_OBJ, 0>, S::XT);
+  a((const void *)k_x2<L, X2_OBJ, 1>, S::XT);
+  a((const void *)k_x2<L, X2_OBJ, 2>, S::XT);
   a((const void *)k_x2<L, X2_FWD>, S::XT);
   a((const void *)k_x2<L, X2_ADJ>, S::XT);
-  a((const void *)k_x2<L, X2_OBJ>, S::XT);
   a((const void *)k_y2<L, false>, S::XPT);
   a((const void *)k_y2<L, true>, S::XPT);
   a((const void *)k_x3<L>, S::XPT);
@@ -66,7 +70,9 @@ void set_ref_attrs() {
   a((const void *)k_ref_rows<L, REF_FINAL>);
   a((const void *)k_ref_rows<L, REF_FWD>);
   a((const void *)k_ref_rows<L, REF_INIT>);
-  a((const void *)k_ref_r2b<L>);
+  a((const void *)k_ref_r2b<L, 0>);
+  a((const void *)k_ref_r2b<L, 1>);
+  a((const void *)k_ref_r2b<L, 2>);
   const int sza = (int)LineEng<L>::SMEM_ACC;
   cudaFuncSetAttribute((const void *)k_ref_r1b<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, sza);
   cudaFuncSetAttribute((const void *)k_ref_r3b<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, sza);
@@ -219,6 +225,7 @@ struct Run {
     const double fl = fftf(L), rN = (double)N / L, NN8 = 8.0 * N * N;
     const bool gq_pass = want_q && (mode == 0 || mode == 2);
     const int fo_ = p->fourier ? 1 : 0;  // holo_set_fourier: psi / eta / grad_psi are DFT2 of the object arrays
+    const int tm_ = p->tau == 1.f ? 0 : (p->tau == 2.f ? 1 : 2);  // residual branch compiled into X2
     int nmag = 0;
     for (int j = 0; j < nz; j++) nmag += (p->magmask >> j) & 1;
     if (ps) {
@@ -329,14 +336,14 @@ struct Run {
           continue;
         }
         if (mode == 3) {
-          k_x2<L, X2_OBJ><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, sqrt_d + fo * NN, nz * NN, nullptr, 0, pf,
-                                                         nz * nbx2, tb, qh, N, p->tau);
+          (tm_ == 0 ? k_x2<L, X2_OBJ, 0> : tm_ == 1 ? k_x2<L, X2_OBJ, 1> : k_x2<L, X2_OBJ, 2>)<<<g2, NT, SM::XT, p->stream>>>(
+              p->W1, NL, sqrt_d + fo * NN, nz * NN, nullptr, 0, pf, nz * nbx2, tb, qh, N, p->tau);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8 / 2), nb * N * fl * 2);
           continue;
         }
         if (mode == 0) {
-          k_x2<L, X2_GRAD><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, sqrt_d + fo * NN, nz * NN, p->V1, NL, pf,
-                                                          nz * nbx2, tb, qh, N, p->tau);
+          (tm_ == 0 ? k_x2<L, X2_GRAD, 0> : tm_ == 1 ? k_x2<L, X2_GRAD, 1> : k_x2<L, X2_GRAD, 2>)<<<g2, NT, SM::XT, p->stream>>>(
+              p->W1, NL, sqrt_d + fo * NN, nz * NN, p->V1, NL, pf, nz * nbx2, tb, qh, N, p->tau);
           pend(p, HOLO_PASS_X2, nb * (2 * rN * A + NN8 / 2), nb * N * fl * 4);
         } else {
           k_x2<L, X2_ADJ><<<g2, NT, SM::XT, p->stream>>>(yin + fo * NN, nz * NN, nullptr, 0, p->V1, NL, pf,
@@ -522,8 +529,9 @@ struct RefRun {
       k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, tw3, N);
       if (staged) cudaStreamWaitEvent(p->stream, p->stage_ev[r0 / p->BR], 0);
       if constexpr (E::HOLD_SMEM) {  // LineEng<6144>: one row of every frame of the batch per CTA (gn == N)
-        k_ref_r2b<L><<<gn, E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
-                                                    p->partR + (size_t)r0 * gn, H, tw, tw3, N, nb, p->tau);
+        const int tm = p->tau == 1.f ? 0 : (p->tau == 2.f ? 1 : 2);
+        (tm == 0 ? k_ref_r2b<L, 0> : tm == 1 ? k_ref_r2b<L, 1> : k_ref_r2b<L, 2>)<<<gn, E::NT, SM, p->stream>>>(
+            p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr, p->partR + (size_t)r0 * gn, H, tw, tw3, N, nb, p->tau);
       } else {
         k_ref_rows<L, REF_R2><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, sqrt_dref + (size_t)r0 * N * N, p->Vr,
                                                                         p->partR + (size_t)r0 * gn, H, tw, tw3, N, 1.f,
