@@ -229,11 +229,13 @@ holo_status holo_init_psi(holo_plan *p, const float *sqrt_d, const float *sqrt_d
  * is dev_sqrt_d first copies host_sqrt_d (PINNED host memory, [K][nz][n][n] float32) into it, one angle
  * batch at a time on a plan-owned copy stream that starts after everything already queued on the
  * plan's stream; each batch's residual pass waits only for its own slice, so the transfer of batch
- * b + 1 overlaps the passes of batch b.  Later calls read the resident data.  NULL pointers cancel a
- * pending stage.  The host buffer must stay valid until that call's work has completed. */
+ * b + 1 overlaps the passes of batch b.  Later calls read the resident data.  A stage stays pending
+ * until a call reads dev_sqrt_d (or it is replaced); NULL pointers cancel it.  The host buffer must stay
+ * valid until that call's work has completed. */
 holo_status holo_stage_sqrt_d(holo_plan *p, const float *host_sqrt_d, float *dev_sqrt_d);
-/* The same for the reference frames (sqrt_dref [R][n][n] of holo_grad_ref / holo_grad_full): streamed per
- * batch of reference frames, each batch's row pass (R2) waiting for its own slice. */
+/* The same for the reference frames (sqrt_dref [R][n][n] of holo_grad_ref / holo_grad_full, R = n_ref of
+ * holo_set_ref_shifts, which must precede it): streamed per batch of reference frames, each batch's row
+ * pass (R2) waiting for its own slice. */
 holo_status holo_stage_sqrt_dref(holo_plan *p, const float *host_sqrt_dref, float *dev_sqrt_dref);
 
 /* Fourier-domain object state (Parseval; SURVEY 8(e) "run CG ... in the Fourier domain").
@@ -248,7 +250,8 @@ holo_status holo_stage_sqrt_dref(holo_plan *p, const float *host_sqrt_dref, floa
  * HOLO_EUNSUPPORTED for npad 6144.
  * holo_fourier: out[m] = DFT2(in[m]) (inverse = 0) or IDFT2(in[m]) = (1/npad^2) sum e^{+...} (inverse = 1)
  * for m < count, row-major [count][npad][npad] complex64; in == out allowed (the plan's scratch sits
- * between the two passes).  Not usable while a sweep of the same plan is pending on another stream. */
+ * between the two passes).  Not usable while a sweep of the same plan is pending on another stream;
+ * HOLO_EUNSUPPORTED on a plan without angles (it uses the object chain's scratch). */
 holo_status holo_set_fourier(holo_plan *p, int32_t on);
 holo_status holo_fourier(holo_plan *p, const void *in, void *out, int32_t count, int32_t inverse);
 

@@ -726,6 +726,7 @@ holo_status holo_fourier(holo_plan *p, const void *in, void *out, int32_t count,
   if (count < 0 || (count > 0 && (!in || !out))) return fail(p, HOLO_EINVAL, "bad holo_fourier arguments");
   if (!p->ops->dft2) return fail(p, HOLO_EUNSUPPORTED, "holo_fourier needs a power-of-two npad");
   if (count == 0) return HOLO_OK;
+  if (p->K == 0) return fail(p, HOLO_EUNSUPPORTED, "holo_fourier needs a plan with angles (object-chain scratch)");
   p->ops->dft2(p, (const float2 *)in, (float2 *)out, count, inverse != 0);
   return postcheck(p);
 }
