@@ -173,8 +173,11 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB)
 // FS = R + T values, ref_factors on the host), so a frame costs one table value per thread plus
 // R warp-uniform (L1 broadcast) values instead of a length-L table.
 // R1B: the Qhat column x hz is read ONCE; per frame: x ramp_b, inverse along y, rows [o, o+N) -> W_b
-template <int L>
-__global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
+#ifndef HOLO_R1B_REREAD
+#define HOLO_R1B_REREAD 1  // re-read the Qhat column (L2) every frame instead of holding it: 3 CTAs / SM (measured +7 %)
+#endif
+template <int L, bool RR = (HOLO_R1B_REREAD && LineEng<L>::HOLD_SMEM)>
+__global__ void __launch_bounds__(LineEng<L>::NT, RR ? LineEng<L>::MINB : LineEng<L>::MINB_ACC)
     k_ref_r1b(const float2 *__restrict__ Qhat, float2 *__restrict__ W, const float2 *__restrict__ hz,
               const float2 *__restrict__ fac, int nb, const float4 *__restrict__ tw, const float2 *__restrict__ tw3,
               int N) {
@@ -185,11 +188,13 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
   const int o = (L - N) / 2;
   float2 q0[E::HOLD_SMEM ? 1 : E::R];
   float2 *hold = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sm4) + E::SMEM) + threadIdx.x;
+  if constexpr (!RR) {
 #pragma unroll
-  for (int r = 0; r < E::R; r++) {  // the frame-independent part Qhat h_{zeta0} / L of the column
-    const int f = E::ifr(st, r);
-    const float2 a = cmul(ldg2(Qhat + p2(f, col, L)), ldg2(hz + f));
-    if constexpr (E::HOLD_SMEM) hold[r * E::NT] = a; else q0[r] = a;
+    for (int r = 0; r < E::R; r++) {  // the frame-independent part Qhat h_{zeta0} / L of the column
+      const int f = E::ifr(st, r);
+      const float2 a = cmul(ldg2(Qhat + p2(f, col, L)), ldg2(hz + f));
+      if constexpr (E::HOLD_SMEM) hold[r * E::NT] = a; else q0[r] = a;
+    }
   }
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
@@ -197,7 +202,16 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
     const float2 Bt = ldg2(A + E::R + st.t);
     float2 v[E::R];
 #pragma unroll
-    for (int r = 0; r < E::R; r++) v[r] = cmul(E::HOLD_SMEM ? hold[r * E::NT] : q0[r], cmul(ldg2(A + r), Bt));
+    for (int r = 0; r < E::R; r++) {
+      float2 qh;
+      if constexpr (RR) {
+        const int f = E::ifr(st, r);
+        qh = cmul(ldg2(Qhat + p2(f, col, L)), ldg2(hz + f));
+      } else {
+        qh = E::HOLD_SMEM ? hold[r * E::NT] : q0[r];
+      }
+      v[r] = cmul(qh, cmul(ldg2(A + r), Bt));
+    }
     E::inv(v, st, tw, tw3);
     float2 *w = W + (size_t)b * N * L;
 #pragma unroll
@@ -210,8 +224,11 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
 
 // R3B: per frame: pad(V_b col) -> forward along y -> x conj(ramp_b), summed over the batch (registers
 // or the private smem slot), x conj(hz); Ghat (+)= the sum: one read-modify-write of Ghat per batch
-template <int L>
-__global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
+#ifndef HOLO_R3B_RED
+#define HOLO_R3B_RED 0  // 1: every frame adds into Ghat with fire-and-forget L2 reductions (no held sum; measured -10 %)
+#endif
+template <int L, bool RD = (HOLO_R3B_RED && LineEng<L>::HOLD_SMEM)>
+__global__ void __launch_bounds__(LineEng<L>::NT, RD ? LineEng<L>::MINB : LineEng<L>::MINB_ACC)
     k_ref_r3b(const float2 *__restrict__ V, float2 *__restrict__ Ghat, const float2 *__restrict__ hz,
               const float2 *__restrict__ fac, int nb, const float4 *__restrict__ tw, const float2 *__restrict__ tw3,
               int N, int first) {
@@ -220,6 +237,29 @@ __global__ void __launch_bounds__(LineEng<L>::NT, LineEng<L>::MINB_ACC)
   typename E::St st = E::init(reinterpret_cast<float2 *>(sm4));
   const int col = blockIdx.x * E::G + st.g;
   const int o = (L - N) / 2;
+  if constexpr (RD) {  // one owner thread per Ghat element: the same sequential sum, no held batch sum
+#pragma unroll 1
+    for (int b = 0; b < nb; b++) {
+      const float2 *vin = V + (size_t)b * N * L;
+      const float2 *A = fac + (size_t)(2 * b + 1) * E::FS;
+      const float2 Bt = ldg2(A + E::R + st.t);
+      float2 v[E::R];
+#pragma unroll
+      for (int r = 0; r < E::R; r++) {
+        const int row = E::isp(st, r) - o;
+        v[r] = (row >= 0 && row < N) ? ldg2(vin + p2(row, col, N)) : make_float2(0.f, 0.f);
+      }
+      E::fwd(v, st, tw, tw3);
+#pragma unroll
+      for (int r = 0; r < E::R; r++) {
+        const int f = E::ifr(st, r);
+        const float2 a = cmulc(cmulc(v[r], cmul(ldg2(A + r), Bt)), ldg2(hz + f));
+        float2 *p = Ghat + p2(f, col, L);
+        if (first && b == 0) *p = a; else red_add2(p, a);
+      }
+    }
+    return;
+  }
   float2 acc[E::HOLD_SMEM ? 1 : E::R];
   float2 *hold = reinterpret_cast<float2 *>(reinterpret_cast<char *>(sm4) + E::SMEM) + threadIdx.x;
 #pragma unroll

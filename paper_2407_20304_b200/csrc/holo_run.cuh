@@ -447,7 +447,7 @@ struct RefRun {
       const float2 *H = p->Href + (size_t)r0 * 2 * L;
       const float2 *F = p->Hfac + (size_t)r0 * 2 * E::FS;
       pbeg(p);
-      k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, p->tw3, N);
+      k_ref_r1b<L><<<gl, E::NT, (HOLO_R1B_REREAD && E::HOLD_SMEM) ? E::SMEM : E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, p->tw3, N);
       k_ref_rows<L, REF_FWD><<<dim3(gn, nb), E::NT, SM, p->stream>>>(p->Wr, nullptr, w + (size_t)r0 * N * N, nullptr, H,
                                                                        tw, p->tw3, N, 1.f, 0);
       pend(p, HOLO_PASS_REF, A + nb * (A + 8.0 * N * N), nb * fl * (L + N), 2);
@@ -472,7 +472,7 @@ struct RefRun {
       pbeg(p);
       k_ref_rows<L, REF_INIT><<<dim3(gn, nb), E::NT, SM, p->stream>>>(nullptr, sqrt_dref + r0 * NN, p->Vr,
                                                                         p->partR + r0, H, tw, p->tw3, N, 1.f, 0);
-      k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, p->hz, F, nb, tw, p->tw3, N, r0 == 0);
+      k_ref_r3b<L><<<gl, E::NT, (HOLO_R3B_RED && E::HOLD_SMEM) ? E::SMEM : E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, p->hz, F, nb, tw, p->tw3, N, r0 == 0);
       pend(p, HOLO_PASS_REF, nb * A * (0.0625 + 0.5 + 0.5) + A * (r0 ? 2.0 : 1.0), nb * fl * (N + L), 2);
     }
     pbeg(p);
@@ -526,7 +526,7 @@ struct RefRun {
       const float2 *F = p->Hfac + (size_t)r0 * 2 * E::FS;
       const bool f0 = first && r0 == 0;
       pbeg(p);
-      k_ref_r1b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, tw3, N);
+      k_ref_r1b<L><<<gl, E::NT, (HOLO_R1B_REREAD && E::HOLD_SMEM) ? E::SMEM : E::SMEM_ACC, p->stream>>>(p->Qhat, p->Wr, p->hz, F, nb, tw, tw3, N);
       if (staged) cudaStreamWaitEvent(p->stream, p->stage_ev[r0 / p->BR], 0);
       if constexpr (E::HOLD_SMEM) {  // LineEng<6144>: one row of every frame of the batch per CTA (gn == N)
         const int tm = p->tau == 1.f ? 0 : (p->tau == 2.f ? 1 : 2);
@@ -537,7 +537,7 @@ struct RefRun {
                                                                         p->partR + (size_t)r0 * gn, H, tw, tw3, N, 1.f,
                                                                         0, p->tau);
       }
-      if (want_q) k_ref_r3b<L><<<gl, E::NT, E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, p->hz, F, nb, tw, tw3, N, f0);
+      if (want_q) k_ref_r3b<L><<<gl, E::NT, (HOLO_R3B_RED && E::HOLD_SMEM) ? E::SMEM : E::SMEM_ACC, p->stream>>>(p->Vr, p->Ghat, p->hz, F, nb, tw, tw3, N, f0);
       // bytes: Qhat once, W write + read, sqrt_d, V write + read per frame, Ghat once per batch
       pend(p, HOLO_PASS_REF,
            A + nb * A * (0.5 + 0.5 + 1.0 / 8 + 0.5 + (want_q ? 0.5 : 0.0)) + (want_q ? A * (f0 ? 1.0 : 2.0) : 0.0),
