@@ -375,6 +375,8 @@ def main():
     ap.add_argument("--multires-angles", type=int, default=16,
                     help="angles of the timed 3-level multiresolution run (SURVEY 8(f) row 3); 0 = skip")
     ap.add_argument("--multires-iters", type=int, default=3, help="CG iterations per level of that run")
+    ap.add_argument("--probe-shifts", type=float, default=0.0,
+                    help="per-frame probe shifts s^p ~ U[-S, S] px (SURVEY 8(f) row 1, holo_set_probe_shifts); 0 = off")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -399,6 +401,10 @@ def main():
                        angle_batch=min(args.batch, K))
         plan.set_shifts(synth.shifts(cfg)[k0:k0 + K] if k0 + K <= cfg.n_angles else
                         np.resize(synth.shifts(cfg), (k0 + K, cfg.nz, 2))[k0:k0 + K])
+        if args.probe_shifts > 0:  # the f-1 path: q_kj = P_omega S_{s^p_kj} q in the data and in every sweep
+            sp = np.random.default_rng([240720304, 7, rank]).uniform(-args.probe_shifts, args.probe_shifts,
+                                                                    size=(K, cfg.nz, 2))
+            plan.set_probe_shifts(sp)
         # ---- synthetic measurement: |forward(truth)|^2 with Poisson noise (bench input, not a parity value)
         q_t = synth.probe(cfg, device=dev, dtype=torch.complex64)
         psi_t = synth.psi_stack(cfg, K=K, device=dev, dtype=torch.complex64, k0=k0)
@@ -421,6 +427,7 @@ def main():
                 "angles_per_gpu": K, "angles_total": K_total, "distances": cfg.nz, "n": cfg.n,
                 "npad": cfg.npad, "rho_q": rho_q, "angle_batch": plan.angle_batch,
                 "parallelism": f"angle-sharded dp{world}",
+                "probe_shifts": args.probe_shifts or None,
                 "l2": "inputs > L2 (each step streams >= 25 GB per GPU; no flush needed)"}
     solver.start()
     for _ in range(args.warmup):

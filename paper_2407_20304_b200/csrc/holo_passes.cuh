@@ -496,7 +496,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // ----------------------------------------------------------------------------- XQ, XG (PS)
 // Per-frame probe shifts (O19): with Qhat = DFT2 q (P2 [fy][fx]) and Hq(k,j) = h_omega_j r_{s^p_kj} / L
 // per axis, q_kj = IDFT_y(Hq_y IDFT_x(Hq_x Qhat)).
-// XQ (rows fy, one angle): Qt_j row = IFFT_x(Hq_x(k, j) Qhat row) for every plane j   (P2 [fy][x])
+// XQ (rows fy, the angles of a batch): Qt[m] row = IFFT_x(Hq_x(k, j) Qhat row) for the m = b nz + j
+// (angle, plane) pairs of the batch (nz argument = their count), Qhat row read once   (P2 [fy][x])
 template <int L>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_xq(const float2 *__restrict__ Qhat, float2 *__restrict__ Qt, Tables tb, const __grid_constant__ TabSeq seq,
@@ -529,7 +530,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   }
 }
 
-// XG (rows fy, one angle): Ghat row (+)= sum_j conj(Hq_x(k, j)) FFT_x(Ut_j row)   (first: overwrite)
+// XG (rows fy, the angles of a batch): Ghat row (+)= sum_m conj(Hq_x(k, j)) FFT_x(Ut[m] row) over the
+// m = b nz + j pairs (nz argument = their count), one Ghat read-modify-write per batch   (first: overwrite)
 template <int L>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_xg(const float2 *__restrict__ Ut, float2 *__restrict__ Ghat, Tables tb, const __grid_constant__ TabSeq seq,

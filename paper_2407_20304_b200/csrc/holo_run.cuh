@@ -282,13 +282,14 @@ struct Run {
           k_x1<L><<<L / G, NT, SM::XPT, p->stream>>>(psi + (size_t)k * LL, p->T1 + (size_t)b * nz * LL, tb, q, nz,
                                                       p->magmask, fo_);
           pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * ((fo_ ? 0 : 1) + 4 * nmag + (nz - nmag)));
-          if (ps) {
-            TabSeq qq{};
-            for (int j = 0; j < nz; j++) qq.p[qq.n++] = hqp(k, j, 0);
-            pbeg(p);
-            k_xq<L><<<L / G, NT, SM::XPT, p->stream>>>(p->Qhat, p->Qt + (size_t)b * nz * LL, tb, qq, nz);
-            pend(p, HOLO_PASS_PS, (1 + nz) * A, L * fl * nz);
-          }
+        }
+        if (ps) {  // XQ for the whole batch: the Qhat row read once, nb x nz row transforms per CTA
+          TabSeq qq{};
+          for (int b = 0; b < nb; b++)
+            for (int j = 0; j < nz; j++) qq.p[qq.n++] = hqp(k0 + b, j, 0);
+          pbeg(p);
+          k_xq<L><<<L / G, NT, SM::XPT, p->stream>>>(p->Qhat, p->Qt, tb, qq, nz * nb);
+          pend(p, HOLO_PASS_PS, (1 + nz * nb) * A, L * fl * nz * nb);
         }
       }
       for (int j = 0; j < nz; j++) {
@@ -386,13 +387,13 @@ struct Run {
       // or the final IDFT2) and p->gq_event recorded, so a caller can allreduce g_q on another
       // stream while this batch's X3 passes run (SURVEY 8e overlap).
       const bool last_batch = k0 + nb >= K;
-      auto xg = [&](int b) {
-        const int k = k0 + b;
+      auto xg = [&]() {  // the whole batch: nb x nz row transforms summed per CTA, one Ghat update per batch
         TabSeq qg{};
-        for (int j = 0; j < nz; j++) qg.p[qg.n++] = hqp(k, j, 0);
+        for (int b = 0; b < nb; b++)
+          for (int j = 0; j < nz; j++) qg.p[qg.n++] = hqp(k0 + b, j, 0);
         pbeg(p);
-        k_xg<L><<<L / G, NT, SM::XPT, p->stream>>>(p->Ut + (size_t)b * nz * LL, p->Ghat, tb, qg, nz, k == 0);
-        pend(p, HOLO_PASS_PS, (nz + (k ? 2 : 1)) * A, L * fl * nz);
+        k_xg<L><<<L / G, NT, SM::XPT, p->stream>>>(p->Ut, p->Ghat, tb, qg, nz * nb, k0 == 0);
+        pend(p, HOLO_PASS_PS, (nz * nb + (k0 ? 2 : 1)) * A, L * fl * nz * nb);
       };
       auto x3 = [&](int b) {
         const int k = k0 + b;
@@ -411,13 +412,11 @@ struct Run {
       };
       const bool want_x3 = gpsi && (mode == 0 || mode == 2);
       if (!last_batch) {
-        for (int b = 0; b < nb; b++) {
-          if (want_x3) x3(b);
-          if (ps && gq_pass) xg(b);
-        }
+        if (want_x3)
+          for (int b = 0; b < nb; b++) x3(b);
+        if (ps && gq_pass) xg();
       } else {
-        if (ps && gq_pass)
-          for (int b = 0; b < nb; b++) xg(b);
+        if (ps && gq_pass) xg();
         finish_q(p, q, gq_out, gscale, want_q, acc_q, mode, sqrt_dref);
         if (want_x3)
           for (int b = 0; b < nb; b++) x3(b);
