@@ -198,6 +198,16 @@ holo_status holo_cg_step(holo_plan *p, const holo_cg_in *in /*[host]*/, holo_cg_
                          const void *psi, void *eta_psi, const void *grad_psi, void *psi_trial,
                          const void *q, void *eta_q, const void *grad_q, void *q_trial);
 
+/* CG-step fusion: holo_set_cg_fuse(p, 1) makes holo_cg_step apply the q block at once but defer the
+ * psi block: the next holo_fwd / holo_adj / holo_grad / holo_grad_full whose psi argument is that call's
+ * psi_trial performs it inside its first row pass (X1 reads the psi, eta_psi and grad_psi rows, writes
+ * the eta_psi and psi_trial rows, and transforms psi_trial) -- the same element-wise arithmetic as the
+ * separate pointwise pass, one pass over the psi block fewer per iteration.  Any other entry point of
+ * the plan first completes a pending update with the separate kernel, so psi_trial / eta_psi are
+ * materialised before anything else of this plan reads them; read them from other code only after
+ * the sweep.  Default 0. */
+holo_status holo_set_cg_fuse(holo_plan *p, int32_t on);
+
 /* Multiresolution schedule ("binning 8x8 ... 4x4 ... then extrapolate
  * the recovered object with the probe function to a grid twice as dense").
  * holo_upsample2: Fourier 2x upsampling (O15, reading R1) of `count` complex64 fields

@@ -105,6 +105,8 @@ _lib.holo_stage_sqrt_d.argtypes = [_P, _P, _P]
 _lib.holo_stage_sqrt_d.restype = _S
 _lib.holo_stage_sqrt_dref.argtypes = [_P, _P, _P]
 _lib.holo_stage_sqrt_dref.restype = _S
+_lib.holo_set_cg_fuse.argtypes = [_P, ctypes.c_int32]
+_lib.holo_set_cg_fuse.restype = _S
 _lib.holo_set_fourier.argtypes = [_P, ctypes.c_int32]
 _lib.holo_set_fourier.restype = _S
 _lib.holo_fourier.argtypes = [_P, _P, _P, ctypes.c_int32, ctypes.c_int32]
@@ -124,7 +126,7 @@ EXPORTED = ["holo_plan_create", "holo_plan_destroy", "holo_plan_workspace_bytes"
             "holo_plan_derived", "holo_set_shifts", "holo_set_ref_shifts", "holo_fwd", "holo_adj", "holo_grad",
             "holo_grad_ref", "holo_fwd_ref", "holo_q_dots", "holo_cg_step", "holo_launch_count", "holo_profile_enable",
             "holo_profile_read", "holo_upsample2", "holo_bin2", "holo_init_probe", "holo_init_psi",
-            "holo_set_probe_shifts", "holo_grad_full", "holo_set_gq_event", "holo_set_tau", "holo_set_fourier", "holo_fourier", "holo_stage_sqrt_d", "holo_stage_sqrt_dref"]
+            "holo_set_probe_shifts", "holo_grad_full", "holo_set_gq_event", "holo_set_tau", "holo_set_fourier", "holo_fourier", "holo_stage_sqrt_d", "holo_stage_sqrt_dref", "holo_set_cg_fuse"]
 
 
 class HoloError(RuntimeError):
@@ -262,6 +264,10 @@ class Plan:
         self._stage_host = host
         self._chk(_lib.holo_stage_sqrt_dref(self._h, ctypes.c_void_p(host.data_ptr()),
                                             _ptr(dev, torch.float32, host.numel(), "dev")))
+
+    def set_cg_fuse(self, on):
+        """holo_set_cg_fuse: defer holo_cg_step's psi-block update into the next sweep's X1."""
+        self._chk(_lib.holo_set_cg_fuse(self._h, int(bool(on))))
 
     def set_fourier(self, on):
         """holo_set_fourier: object-side arrays of later fwd / adj / grad calls are DFT2(psi) (unnormalised)."""

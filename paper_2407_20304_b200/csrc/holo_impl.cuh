@@ -60,6 +60,12 @@ struct holo_plan {
   // Qt [B][nz][L][L] (IDFT_x(Hq_x Qhat), P2), Qk [B][L][L] (q_kj, P2), Ut [B][nz][L][L] (probe-gradient terms)
   bool ps = false;
   bool fourier = false;  // holo_set_fourier: the object-side arrays are DFT2(psi) (Fourier-domain CG state)
+  // holo_set_cg_fuse: the psi-block half of holo_cg_step deferred into the next sweep's X1
+  bool cg_fuse = false, cg_pending = false;
+  const float2 *cg_psi = nullptr, *cg_g = nullptr;
+  float2 *cg_eta = nullptr, *cg_trial = nullptr;
+  float cg_rho = 0.f, cg_beta = 0.f, cg_gamma = 0.f;
+  int cg_mode = -1;
   // holo_stage_sqrt_d: a pending host -> device copy of the data, streamed per angle batch on a copy
   // stream by the next sweep that reads stage_dev (each batch's X2 waits for its own event)
   const float *stage_host = nullptr;
@@ -116,6 +122,7 @@ struct HoloOps {
 };
 
 const HoloOps *holo_ops_for(int L);  // NULL if L is not built
+void holo_cg_flush(holo_plan *p);     // launch a deferred psi-block CG update (holo_set_cg_fuse) now
 
 // ------------------------------------------------------------------ profiling
 // pbeg / pend bracket one pass (one or more kernels); pend counts `nk` launches.

@@ -85,10 +85,20 @@ __device__ __noinline__ TabPipe<L> x1_plane(float2 *__restrict__ T1j, const floa
   return pipe;
 }
 
+// The psi-block CG update fused into X1 (holo_set_cg_fuse): mode -1 off; otherwise the row of
+// x_trial = x + gamma eta with eta = -rho g (mode 0), -rho g + beta eta (mode 1) or eta (mode 2),
+// written to trial (and eta), is the row X1 transforms -- the arithmetic of k_cg, element by element.
+struct CgFuse {
+  const float2 *g;
+  float2 *eta, *trial;
+  float rho, beta, gamma;
+  int mode;
+};
+
 template <int L>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x1(const float2 *__restrict__ psi_k, float2 *__restrict__ T1, Tables tb, const __grid_constant__ TabSeq seq,
-         int nz, uint32_t magmask, int fourier) {
+         int nz, uint32_t magmask, int fourier, CgFuse cg) {
   using C = CtaK<L>;
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
@@ -101,6 +111,28 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     const int t = C::t(), y = blockIdx.x * C::G + C::g();
     float2 v[16];
     ld_row<L>(v, psi_k + (size_t)y * L, t);
+    if (cg.mode >= 0) {
+      const size_t row = (size_t)y * L;
+#pragma unroll
+      for (int r = 0; r < 16; r++) {
+        const size_t i = row + t + r * (L / 16);
+        float2 e;
+        if (cg.mode == 2) {
+          e = cg.eta[i];
+        } else {
+          const float2 gv = ldg2(cg.g + i);
+          if (cg.mode == 0) {
+            e = make_float2(-cg.rho * gv.x, -cg.rho * gv.y);
+          } else {
+            const float2 ev = cg.eta[i];
+            e = make_float2(fmaf(cg.beta, ev.x, -cg.rho * gv.x), fmaf(cg.beta, ev.y, -cg.rho * gv.y));
+          }
+          cg.eta[i] = e;
+        }
+        v[r] = make_float2(fmaf(cg.gamma, e.x, v[r].x), fmaf(cg.gamma, e.y, v[r].y));
+        cg.trial[i] = v[r];
+      }
+    }
     if (!fourier) fft<L, false>(v, x, t, tb.tw);  // HOLO_FOURIER: the row of DFT2(psi) IS the x-spectrum
 #pragma unroll
     for (int r = 0; r < 16; r++) X[r] = v[r];

@@ -196,11 +196,13 @@ holo_status upload_cr(holo_plan *p, const double *s) {
 
 holo_status ensure_fourier_ws(holo_plan *p);  // below
 
-holo_status precheck(holo_plan *p) {
+// keep_cg: the sweep entry points decide themselves whether a deferred CG step fuses into their X1
+holo_status precheck(holo_plan *p, bool keep_cg = false) {
   if (!p) return HOLO_EINVAL;
   if (p->sticky) return fail(p, HOLO_ESTATE, "plan is in an error state: " + p->err);
   cudaError_t e = cudaSetDevice(p->device);
   if (e != cudaSuccess) return cuda_check(p, e, "cudaSetDevice");
+  if (p->cg_pending && !keep_cg) holo_cg_flush(p);
   return HOLO_OK;
 }
 
@@ -209,6 +211,17 @@ holo_status postcheck(holo_plan *p) { return cuda_check(p, cudaGetLastError(), "
 }  // namespace
 
 // =================================================================== C ABI
+void holo_cg_flush(holo_plan *p) {
+  if (!p->cg_pending) return;
+  p->cg_pending = false;
+  const size_t LL = (size_t)p->L * p->L;
+  const int mode = p->cg_mode;
+  pbeg(p);
+  k_cg<<<1184, 256, 0, p->stream>>>((const float4 *)p->cg_psi, (float4 *)p->cg_eta, (const float4 *)p->cg_g,
+                                    (float4 *)p->cg_trial, LL * p->K / 2, p->cg_rho, p->cg_beta, p->cg_gamma, mode);
+  pend(p, HOLO_PASS_CG, 8.0 * LL * p->K * (mode == 2 ? 3 : mode == 0 ? 4 : 5), 0);
+}
+
 extern "C" {
 
 holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device, void *stream) {
@@ -498,7 +511,7 @@ holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
 }
 
 holo_status holo_fwd(holo_plan *p, const void *psi, const void *q, void *w) {
-  holo_status st = precheck(p);
+  holo_status st = precheck(p, true);
   if (st != HOLO_OK) return st;
   if (!psi || !q || !w) return fail(p, HOLO_EINVAL, "null pointer");
   if (p->K == 0) return HOLO_OK;
@@ -508,7 +521,7 @@ holo_status holo_fwd(holo_plan *p, const void *psi, const void *q, void *w) {
 }
 
 holo_status holo_adj(holo_plan *p, const void *y, const void *psi, const void *q, void *adj_psi, void *adj_q) {
-  holo_status st = precheck(p);
+  holo_status st = precheck(p, true);
   if (st != HOLO_OK) return st;
   if (!y || !psi || !q) return fail(p, HOLO_EINVAL, "null pointer");
   if (!adj_psi && !adj_q) return HOLO_OK;
@@ -577,14 +590,14 @@ extern "C" {
 
 holo_status holo_grad(holo_plan *p, const void *psi, const void *q, const float *sqrt_d, const void *eta_psi_prev,
                       void *grad_psi, void *grad_q_part, double *sc, uint32_t flags) {
-  holo_status st = precheck(p);
+  holo_status st = precheck(p, true);
   if (st != HOLO_OK) return st;
   return grad_impl(p, psi, q, sqrt_d, nullptr, eta_psi_prev, grad_psi, grad_q_part, sc, flags);
 }
 
 holo_status holo_grad_full(holo_plan *p, const void *psi, const void *q, const float *sqrt_d, const float *sqrt_dref,
                            const void *eta_psi_prev, void *grad_psi, void *grad_q_part, double *sc, uint32_t flags) {
-  holo_status st = precheck(p);
+  holo_status st = precheck(p, true);
   if (st != HOLO_OK) return st;
   return grad_impl(p, psi, q, sqrt_d, sqrt_dref, eta_psi_prev, grad_psi, grad_q_part, sc, flags);
 }
@@ -712,6 +725,13 @@ holo_status holo_stage_sqrt_dref(holo_plan *p, const float *host_sqrt_dref, floa
   return stage_impl(p, host_sqrt_dref, dev_sqrt_dref, true);
 }
 
+holo_status holo_set_cg_fuse(holo_plan *p, int32_t on) {
+  holo_status st = precheck(p);  // completes a pending update first
+  if (st != HOLO_OK) return st;
+  p->cg_fuse = on != 0;
+  return HOLO_OK;
+}
+
 holo_status holo_set_fourier(holo_plan *p, int32_t on) {
   holo_status st = precheck(p);
   if (st != HOLO_OK) return st;
@@ -804,12 +824,17 @@ holo_status holo_cg_step(holo_plan *p, const holo_cg_in *in, holo_cg_out *out, c
   out->g_eta_new = gen;
   out->reset = reset;
   const size_t LL = (size_t)p->L * p->L;
-  if (psi && eta_psi && psi_trial && (grad_psi || mode == 2)) {
-    pbeg(p);
-    k_cg<<<1184, 256, 0, p->stream>>>((const float4 *)psi, (float4 *)eta_psi, (const float4 *)grad_psi,
-                                      (float4 *)psi_trial, LL * p->K / 2, (float)in->rho_psi, (float)beta,
-                                      (float)in->gamma, mode);
-    pend(p, HOLO_PASS_CG, 8.0 * LL * p->K * (mode == 2 ? 3 : mode == 0 ? 4 : 5), 0);
+  if (psi && eta_psi && psi_trial && (grad_psi || mode == 2) && p->K > 0) {
+    p->cg_psi = (const float2 *)psi;
+    p->cg_g = (const float2 *)grad_psi;
+    p->cg_eta = (float2 *)eta_psi;
+    p->cg_trial = (float2 *)psi_trial;
+    p->cg_rho = (float)in->rho_psi;
+    p->cg_beta = (float)beta;
+    p->cg_gamma = (float)in->gamma;
+    p->cg_mode = mode;
+    p->cg_pending = true;
+    if (!p->cg_fuse) holo_cg_flush(p);  // otherwise the next sweep at psi_trial runs it inside X1
   }
   if (q && eta_q && q_trial && (grad_q || mode == 2)) {
     pbeg(p);

@@ -248,6 +248,18 @@ struct Run {
       for (auto *e : list) q.p[q.n++] = e;
     };
     const bool need_fwd_chain = (mode != 2) || want_q || ps;
+    // a deferred psi-block CG step (holo_set_cg_fuse) whose trial point is this sweep's psi runs inside X1
+    CgFuse cgf{nullptr, nullptr, nullptr, 0.f, 0.f, 0.f, -1};
+    const float2 *psi_src = psi;
+    if (p->cg_pending) {
+      if (need_fwd_chain && psi == p->cg_trial && K > 0) {
+        cgf = CgFuse{p->cg_g, p->cg_eta, p->cg_trial, p->cg_rho, p->cg_beta, p->cg_gamma, p->cg_mode};
+        psi_src = p->cg_psi;
+        p->cg_pending = false;
+      } else {
+        holo_cg_flush(p);
+      }
+    }
     // holo_stage_sqrt_d: stream the data in per angle batch on the copy stream (after everything
     // queued so far on the plan's stream, i.e. the previous readers of the device buffer), so batch
     // b + 1's copy overlaps batch b's passes; batch b's first X2 waits for its own event
@@ -279,9 +291,16 @@ struct Run {
               q.p[q.n++] = crp(k, j, 0);
           }
           pbeg(p);
-          k_x1<L><<<L / G, NT, SM::XPT, p->stream>>>(psi + (size_t)k * LL, p->T1 + (size_t)b * nz * LL, tb, q, nz,
-                                                      p->magmask, fo_);
-          pend(p, HOLO_PASS_X1, (1 + nz) * A, L * fl * ((fo_ ? 0 : 1) + 4 * nmag + (nz - nmag)));
+          CgFuse cgk = cgf;
+          if (cgk.mode >= 0) {
+            if (cgk.g) cgk.g += (size_t)k * LL;
+            cgk.eta += (size_t)k * LL;
+            cgk.trial += (size_t)k * LL;
+          }
+          k_x1<L><<<L / G, NT, SM::XPT, p->stream>>>(psi_src + (size_t)k * LL, p->T1 + (size_t)b * nz * LL, tb, q,
+                                                      nz, p->magmask, fo_, cgk);
+          pend(p, HOLO_PASS_X1, (1 + nz + (cgk.mode < 0 ? 0 : cgk.mode == 2 ? 2 : cgk.mode == 0 ? 3 : 4)) * A,
+               L * fl * ((fo_ ? 0 : 1) + 4 * nmag + (nz - nmag)));
         }
         if (ps) {  // XQ for the whole batch: the Qhat row read once, nb x nz row transforms per CTA
           TabSeq qq{};

@@ -27,7 +27,8 @@ class JointCG:
     a plan with n_angles = 0 then runs the probe-only problem of configs[4] (rho_psi unused)."""
 
     def __init__(self, plan, sqrt_d, psi0, q0, rho_psi=1.0, rho_q=1.0, gamma_init=1.0, max_halvings=12,
-                 group=None, distributed=None, sqrt_dref=None, fused=None, overlap=True, fourier=None):
+                 group=None, distributed=None, sqrt_dref=None, fused=None, overlap=True, fourier=None,
+                 fuse_cg=None):
         self.plan = plan
         self.d = sqrt_d
         self.dref = sqrt_dref
@@ -55,6 +56,12 @@ class JointCG:
         self._psi, self.q = psi0.contiguous().clone(), q0.contiguous().clone()
         if self.fourier:
             plan.fourier(self._psi)
+        # holo_set_cg_fuse: the psi-block half of every CG step runs inside the following sweep's X1
+        # (correct and bit-identical, but measured slower at cfg3: X1 +40 us/frame > the 28 us/frame
+        # pointwise pass it replaces), so off unless asked for
+        self.fuse_cg = bool(fuse_cg)
+        if hasattr(plan, "set_cg_fuse") and psi0.numel() > 0:
+            plan.set_cg_fuse(self.fuse_cg)
         self.psi_t, self.q_t = z(self._psi), z(self.q)
         self.eta_psi, self.eta_q = z(self._psi), z(self.q)
         self.g_psi, self.g_q = z(self._psi), z(self.q)

@@ -149,3 +149,30 @@ def test_q_dots_full_size_vs_numpy():
     assert abs(o[1] - ref[1]) / abs(ref[1]) < 1e-6
     plan.q_dots(gq, None, out)
     assert host(out).real[1] == 0.0
+
+
+@pytest.mark.parametrize("fourier", [False, True])
+def test_fused_cg_step_bit_identical(fourier):
+    """holo_set_cg_fuse: the psi-block CG update run inside the next sweep's X1 gives the same
+    iterates, bit for bit, as the separate pointwise pass (4 iterations with the line search, cfg0)."""
+    import paper_2407_20304_b200 as hb
+    from paper_2407_20304_b200.solver import JointCG
+    cfg = synth.CONFIGS["cfg0"]
+    K = 4
+    g = oracle.Geometry(cfg.wavelength, cfg.Z, cfg.z1, cfg.det_pixel)
+    psi_t = synth.psi_stack(cfg, K=K).numpy()
+    q_t = synth.probe(cfg).numpy()
+    s = synth.shifts(cfg, K=K)
+    d = synth.poisson_amplitude(np.abs(oracle.fwd(g, psi_t, q_t, s, cfg.n)) ** 2, cfg.photons, cfg)
+    out = []
+    for fuse in (False, True):
+        plan = hb.Plan(cfg.n, cfg.npad, cfg.z1, K, cfg.wavelength, cfg.Z, cfg.det_pixel, device=0, angle_batch=2)
+        plan.set_shifts(s)
+        cg = JointCG(plan, dev(d, torch.float32), dev(np.ones_like(psi_t)), dev(0.9 * q_t), rho_psi=1.0,
+                     rho_q=1.0 / K, distributed=False, fourier=fourier, fuse_cg=fuse)
+        cg.start()
+        hist = [cg.iterate() for _ in range(4)]
+        out.append(([(h["F"], h["gamma"], h["beta"]) for h in hist], host(cg.psi), host(cg.q), host(cg.eta_psi)))
+    assert out[0][0] == out[1][0]
+    for a, b in zip(out[0][1:], out[1][1:]):
+        assert np.array_equal(a, b)
