@@ -428,6 +428,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 }
 
 // ----------------------------------------------------------------------------- X3
+#ifndef HOLO_X3_ZACC
+#define HOLO_X3_ZACC 0  // 1: plane sum in the private slot, source read twice from global (L2)
+#endif
 // rows: g_k row = scale * IFFT( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3_j row;
 // partial[blk][0] = sum |g|^2, partial[blk][1] = sum Re(g conj(eta))   (g, eta row-major)
 // The sum over planes is kept in the g row itself (L2-resident between planes); each plane
@@ -442,6 +445,31 @@ __device__ __noinline__ TabPipe<L> x3_plane(const float2 *__restrict__ T3j, floa
   const Priv<NT> Z{priv_base<L>(sm)};
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 v[16];
+#if HOLO_X3_ZACC
+  // the plane sum stays in the private slot Z; the magnification reads its source twice from
+  // global memory (the second read hits L2)
+  if (mag) {
+    if (!last && (threadIdx.x & 3) == 0) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) prefetch_l2_sector(T3j + (size_t)L * L + p2(y, t + r * T, L));
+    }
+    float2 e[16];
+    mag_adj<L>(
+        v, [&](int r) { return ldg2(T3j + p2(y, t + r * T, L)); }, [&](int r, float2 val) { e[r] = val; },
+        [&](int r) { return e[r]; }, pipe, seq, j > 0, x, t, tw);
+  } else {
+    ld_p2_row<L>(v, T3j, y, L, t);
+    fft<L, false>(v, x, t, tw);
+    const float2 *cr = pipe.take(seq);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
+    pipe.done(seq);
+  }
+#pragma unroll
+  for (int r = 0; r < 16; r++) Z[r] = j == 0 ? v[r] : cadd(Z[r], v[r]);
+  (void)grow;
+  return pipe;
+#endif
   if (mag) {
     // the source row is read ONCE into the thread-private slot; the first half's term is
     // parked in registers (as in X1)
