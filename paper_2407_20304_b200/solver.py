@@ -85,10 +85,17 @@ class JointCG:
 
     @property
     def psi(self):
-        """The object block in the object domain (a converted copy in Fourier mode)."""
+        """The object block in the object domain (in Fourier mode a NEW converted copy, K x npad^2
+        complex64 -- use psi_into(out) to reuse a buffer)."""
         if not self.fourier:
             return self._psi
         return self.plan.fourier(self._psi, torch.empty_like(self._psi), inverse=True)
+
+    def psi_into(self, out):
+        """Write the object-domain psi block into `out` (same shape / dtype as psi0); returns out."""
+        if not self.fourier:
+            return out.copy_(self._psi)
+        return self.plan.fourier(self._psi, out, inverse=True)
 
     # ------------------------------------------------------------------ sweep
     def sweep(self, psi, q, eta_psi, eta_q, g_psi, g_q):
