@@ -429,7 +429,6 @@ holo_status holo_set_ref_shifts(holo_plan *p, int32_t n_ref, const double *s) {
   for (int i = 0; i < 2 * n_ref; i++)
     if (!std::isfinite(s[i]) || std::fabs(s[i]) >= p->L / 2) return fail(p, HOLO_EINVAL, "shift not finite or >= npad/2");
   const int L = p->L, N = p->N;
-  const size_t LL = (size_t)L * L;
   // workspace of the reference arm, allocated on first use (shared with the probe-shift path)
   st = ensure_fourier_ws(p);
   if (st != HOLO_OK) return st;
