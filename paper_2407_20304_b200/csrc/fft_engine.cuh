@@ -53,6 +53,29 @@ namespace holo {
 #endif
 __device__ __forceinline__ int P(int i) { return HOLO_PAD2 ? i + 2 * (i >> 4) : i + (i >> 4); }
 
+// Complex arithmetic.  HOLO_FFMA2=1: Blackwell's packed f32x2 instructions (FADD2 / FMUL2 /
+// FFMA2) on the (re, im) pair, whose operand modifiers swap the halves (.LO_HI), negate one half
+// (.NP) or broadcast a scalar (.F32): a complex multiply is FMUL2 + FFMA2 (2 issue slots instead
+// of 4), a twiddled butterfly 3 FFMA2 instead of 6 FFMA (-35 % FP32 SASS instructions in the
+// engine).  MEASURED SLOWER (tools/fftbench2.cu: 39.2 vs 35.45 us per 4096^2 set at 512 threads;
+// cfg3 sweep 907.6 vs 949.3 frame-it/s, profiles/r02_ffma2.log): the FP32 pipe is bound by lane
+// operations, not by issue slots, so the default stays HOLO_FFMA2=0 (scalar FP32).
+#ifndef HOLO_FFMA2
+#define HOLO_FFMA2 0
+#endif
+#if HOLO_FFMA2
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  // (ax bx - ay by, ax by + ay bx) = ax (bx, by) + ay (-by, bx)
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), b));
+}
+// a * conj(b) = (ax bx + ay by, ay bx - ax by) = ax (bx, -by) + ay (by, bx)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(b.y, b.x), __fmul2_rn(make_float2(a.x, a.x), make_float2(b.x, -b.y)));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
@@ -62,8 +85,9 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
-__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+#endif
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 __device__ __forceinline__ float2 ldg2(const float2 *p) { return __ldg(p); }
 
 // Multiply by W16^e = exp(-+2 pi i e / 16) (forward: minus), e in [0, 8), compile-time.
@@ -147,12 +171,20 @@ __device__ __forceinline__ void dft_reg(float2 *v) {
 
 // (a, b) <- (a + t b, a - t b), runtime twiddle t
 __device__ __forceinline__ void bfly(float2 &a, float2 &b, float2 t) {
+#if HOLO_FFMA2
+  // p = a + tx (bx, by) + ty (-by, bx);  q = 2 a - p      (3 FFMA2, the same roundings per lane)
+  float2 p = __ffma2_rn(make_float2(t.x, t.x), b, a);
+  p = __ffma2_rn(make_float2(t.y, t.y), make_float2(-b.y, b.x), p);
+  b = __ffma2_rn(make_float2(2.f, 2.f), a, make_float2(-p.x, -p.y));
+  a = p;
+#else
   float px = fmaf(t.x, b.x, a.x);
   px = fmaf(-t.y, b.y, px);
   float py = fmaf(t.x, b.y, a.y);
   py = fmaf(t.y, b.x, py);
   b = make_float2(fmaf(2.f, a.x, -px), fmaf(2.f, a.y, -py));
   a = make_float2(px, py);
+#endif
 }
 // (a, b) <- (a + t b, a - t b), t = W16^E (forward, e^{-2 pi i E/16}) or its conjugate (INV)
 template <int E, bool INV>

@@ -167,6 +167,12 @@ __device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// the same for any block: its 16-byte-aligned interior (the bulk copy's alignment rule)
+__device__ __forceinline__ void prefetch_l2_any(const void *src, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src), b = (a + 15) & ~(uintptr_t)15, e = (a + bytes) & ~(uintptr_t)15;
+  if (e > b) prefetch_l2(reinterpret_cast<const void *>(b), (uint32_t)(e - b));
+}
+
 // per-thread L2 prefetch of the sector holding p (no register, no scoreboard)
 __device__ __forceinline__ void prefetch_l2_sector(const void *p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p) : "memory");

@@ -239,31 +239,27 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 }
 
 // ----------------------------------------------------------------------------- X2
-// rows y < N of frame b = blockIdx.y of an nb-frame batch (one plane, so one table set).
+// rows y < N of the nb frames of a batch (one plane, so one transfer table for all of them).
 //   GRAD: W1 row -> D_x, crop, residual (+F), pad, D_x^* -> V1   (W1, V1: P2, N rows)
 //   FWD : W1 row -> D_x, crop -> w frame [N][N] (row-major)
 //   ADJ : y frame row (row-major) -> pad, D_x^* -> V1
 //   OBJ : W1 row -> D_x, crop, F only
 // Strides between the batch's frames: in / out (elements), sqrt_d (elements), partial (CTAs).
-template <int L, int MODE, int TM = -1>
-__global__ void __launch_bounds__(NT, CTAS_PER_SM)
-    k_x2(const float2 *__restrict__ in, size_t in_stride, const float *__restrict__ sqrt_d, size_t d_stride,
-         float2 *__restrict__ out, size_t out_stride, double *__restrict__ partial, int part_stride, Tables tb,
-         const __grid_constant__ TabSeq seq, int N, float tau) {
+// HOLO_X2_LOOP=1 (default): a CTA owns G rows of EVERY frame of the batch (frame loop inside, as
+// Y1 / Y2 do): the table hdet_j / L is bulk-copied into shared memory once per CTA instead of once
+// per (CTA, frame), and the next frame's rows are prefetched into L2 while this frame is
+// transformed, so the row loads stop exposing DRAM latency at every CTA start.
+// HOLO_X2_LOOP=0: one frame per CTA (blockIdx.y), the round-1 launch shape.
+#ifndef HOLO_X2_LOOP
+#define HOLO_X2_LOOP 1
+#endif
+template <int L, int MODE, int TM>
+__device__ __forceinline__ void x2_frame(const float2 *__restrict__ in, const float *__restrict__ sqrt_d,
+                                         float2 *__restrict__ out, double *__restrict__ partial, const float2 *h,
+                                         Xch &x, const float4 *__restrict__ tw, double *red, int N, float tau,
+                                         uint64_t *bar) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
-  extern __shared__ float4 sm4[];
-  __shared__ double red[32];
-  __shared__ uint64_t bars[2];
-  float2 *sm = reinterpret_cast<float2 *>(sm4);
-  Xch x = C::xch(sm);
-  TabPipe<L> pipe;  // hdet_j / L (GRAD: twice)
-  pipe.start(seq, slot_base<L, false>(sm), bars);
-  const int fb = blockIdx.y;
-  in += fb * in_stride;
-  out += fb * out_stride;
-  if (sqrt_d) sqrt_d += fb * d_stride;
-  partial += (size_t)fb * part_stride;
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   const bool act = y < N;
   const int o = (L - N) / 2;
@@ -279,12 +275,11 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   if (MODE != X2_ADJ) {
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = act ? ldg2(in + p2(y, t + r * T, N)) : make_float2(0.f, 0.f);
-    fft<L, false>(v, x, t, tb.tw);
-    const float2 *h = pipe.take(seq);
+    fft<L, false>(v, x, t, tw);
+    mbar_wait(bar, 0);  // the resident table has arrived (returns at once after the first frame)
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], h[t + r * T]);
-    pipe.done(seq);
-    fft<L, true>(v, x, t, tb.tw);
+    fft<L, true>(v, x, t, tw);
     if (MODE == X2_FWD) {
       if (act) {
 #pragma unroll
@@ -315,13 +310,57 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       v[r] = (act && c >= 0 && c < N) ? ldg2(in + (size_t)y * N + c) : make_float2(0.f, 0.f);
     }
   }
-  fft<L, false>(v, x, t, tb.tw);
-  const float2 *h = pipe.take(seq);
+  fft<L, false>(v, x, t, tw);
+  mbar_wait(bar, 0);
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], h[t + r * T]);
-  pipe.done(seq);
-  fft<L, true>(v, x, t, tb.tw);
+  fft<L, true>(v, x, t, tw);
   if (act) st_p2_row<L>(v, out, y, N, t);
+}
+
+template <int L, int MODE, int TM = -1>
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
+    k_x2(const float2 *__restrict__ in, size_t in_stride, const float *__restrict__ sqrt_d, size_t d_stride,
+         float2 *__restrict__ out, size_t out_stride, double *__restrict__ partial, int part_stride, Tables tb,
+         const __grid_constant__ TabSeq seq, int N, float tau, int nb) {
+  using C = CtaK<L>;
+  constexpr int T = L / 16;
+  extern __shared__ float4 sm4[];
+  __shared__ double red[32];
+  __shared__ uint64_t bars[2];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  Xch x = C::xch(sm);
+  // the launch's only table (hdet_j / L; seq.p[0]) into the first slot, once
+  float2 *h = slot_base<L, false>(sm);
+  if (threadIdx.x == 0) {
+    mbar_init(bars, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(bars, L * sizeof(float2));
+    bulk_g2s(h, seq.p[0], L * sizeof(float2), bars);
+  }
+  const int t = C::t(), y0 = blockIdx.x * C::G;
+  const int f0 = HOLO_X2_LOOP ? 0 : blockIdx.y, f1 = HOLO_X2_LOOP ? nb : blockIdx.y + 1;
+#pragma unroll 1
+  for (int fb = f0; fb < f1; fb++) {
+    if (HOLO_X2_LOOP && fb + 1 < f1) {  // the next frame's rows into L2 (one lane per 32-byte sector)
+      if (MODE == X2_ADJ) {
+        if (threadIdx.x == 0 && y0 < N)
+          prefetch_l2_any(in + (fb + 1) * in_stride + (size_t)y0 * N, 8u * N * (y0 + C::G <= N ? C::G : N - y0));
+      } else if ((threadIdx.x & 3) == 0 && y0 + C::g() < N) {
+        const float2 *nx = in + (fb + 1) * in_stride;
+#pragma unroll
+        for (int r = 0; r < 16; r++) prefetch_l2_sector(nx + p2(y0 + C::g(), t + r * T, N));
+      }
+      if ((MODE == X2_GRAD || MODE == X2_OBJ) && threadIdx.x == 32 && y0 < N)
+        prefetch_l2_any(sqrt_d + (fb + 1) * d_stride + (size_t)y0 * N, 4u * N * (y0 + C::G <= N ? C::G : N - y0));
+    }
+    x2_frame<L, MODE, TM>(in + fb * in_stride, sqrt_d ? sqrt_d + fb * d_stride : nullptr,
+                          out ? out + fb * out_stride : nullptr, partial + (size_t)fb * part_stride, h, x, tb.tw, red,
+                          N, tau, bars);
+  }
 }
 
 // ----------------------------------------------------------------------------- Y2

@@ -20,6 +20,7 @@ struct Smem {
   static constexpr size_t X = CtaK<L>::XBYTES;                          // exchange space only (filters)
   static constexpr size_t XT = X + TabPipe<L>::BYTES;                    // + two table slots
   static constexpr size_t XPT = X + CtaK<L>::PRIV + TabPipe<L>::BYTES;  // + one thread-private line
+  static constexpr size_t XH = X + sizeof(float2) * L;                   // + X2's resident table
 };
 
 template <int L>
@@ -35,14 +36,14 @@ void set_chain_attrs() {
   a((const void *)k_y1<L, true>, S::XPT);
   a((const void *)k_xq<L>, S::XPT);
   a((const void *)k_xg<L>, S::XPT);
-  a((const void *)k_x2<L, X2_GRAD, 0>, S::XT);
-  a((const void *)k_x2<L, X2_GRAD, 1>, S::XT);
-  a((const void *)k_x2<L, X2_GRAD, 2>, S::XT);
-  a((const void *)k_x2<L, X2_OBJ, 0>, S::XT);
-  a((const void *)k_x2<L, X2_OBJ, 1>, S::XT);
-  a((const void *)k_x2<L, X2_OBJ, 2>, S::XT);
-  a((const void *)k_x2<L, X2_FWD>, S::XT);
-  a((const void *)k_x2<L, X2_ADJ>, S::XT);
+  a((const void *)k_x2<L, X2_GRAD, 0>, S::XH);
+  a((const void *)k_x2<L, X2_GRAD, 1>, S::XH);
+  a((const void *)k_x2<L, X2_GRAD, 2>, S::XH);
+  a((const void *)k_x2<L, X2_OBJ, 0>, S::XH);
+  a((const void *)k_x2<L, X2_OBJ, 1>, S::XH);
+  a((const void *)k_x2<L, X2_OBJ, 2>, S::XH);
+  a((const void *)k_x2<L, X2_FWD>, S::XH);
+  a((const void *)k_x2<L, X2_ADJ>, S::XH);
   a((const void *)k_y2<L, false>, S::XPT);
   a((const void *)k_y2<L, true>, S::XPT);
   a((const void *)k_x3<L>, S::XPT);
@@ -346,28 +347,28 @@ struct Run {
         TabSeq qh{};
         qh.p[qh.n++] = p->hdet + (size_t)j * L;
         if (mode == 0 || mode == 2) qh.p[qh.n++] = p->hdet + (size_t)j * L;
-        const dim3 g2(nbx2, nb);
+        const dim3 g2(nbx2, HOLO_X2_LOOP ? 1 : nb);
         const size_t fo = (size_t)k0 * nz + j;  // first frame of the batch in [k][j] order
         pbeg(p);
         if (mode == 1) {
-          k_x2<L, X2_FWD><<<g2, NT, SM::XT, p->stream>>>(p->W1, NL, nullptr, 0, wout + fo * NN, nz * NN, pf,
-                                                         nz * nbx2, tb, qh, N, p->tau);
+          k_x2<L, X2_FWD><<<g2, NT, SM::XH, p->stream>>>(p->W1, NL, nullptr, 0, wout + fo * NN, nz * NN, pf,
+                                                         nz * nbx2, tb, qh, N, p->tau, nb);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
           continue;
         }
         if (mode == 3) {
-          (tm_ == 0 ? k_x2<L, X2_OBJ, 0> : tm_ == 1 ? k_x2<L, X2_OBJ, 1> : k_x2<L, X2_OBJ, 2>)<<<g2, NT, SM::XT, p->stream>>>(
-              p->W1, NL, sqrt_d + fo * NN, nz * NN, nullptr, 0, pf, nz * nbx2, tb, qh, N, p->tau);
+          (tm_ == 0 ? k_x2<L, X2_OBJ, 0> : tm_ == 1 ? k_x2<L, X2_OBJ, 1> : k_x2<L, X2_OBJ, 2>)<<<g2, NT, SM::XH, p->stream>>>(
+              p->W1, NL, sqrt_d + fo * NN, nz * NN, nullptr, 0, pf, nz * nbx2, tb, qh, N, p->tau, nb);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8 / 2), nb * N * fl * 2);
           continue;
         }
         if (mode == 0) {
-          (tm_ == 0 ? k_x2<L, X2_GRAD, 0> : tm_ == 1 ? k_x2<L, X2_GRAD, 1> : k_x2<L, X2_GRAD, 2>)<<<g2, NT, SM::XT, p->stream>>>(
-              p->W1, NL, sqrt_d + fo * NN, nz * NN, p->V1, NL, pf, nz * nbx2, tb, qh, N, p->tau);
+          (tm_ == 0 ? k_x2<L, X2_GRAD, 0> : tm_ == 1 ? k_x2<L, X2_GRAD, 1> : k_x2<L, X2_GRAD, 2>)<<<g2, NT, SM::XH, p->stream>>>(
+              p->W1, NL, sqrt_d + fo * NN, nz * NN, p->V1, NL, pf, nz * nbx2, tb, qh, N, p->tau, nb);
           pend(p, HOLO_PASS_X2, nb * (2 * rN * A + NN8 / 2), nb * N * fl * 4);
         } else {
-          k_x2<L, X2_ADJ><<<g2, NT, SM::XT, p->stream>>>(yin + fo * NN, nz * NN, nullptr, 0, p->V1, NL, pf,
-                                                         nz * nbx2, tb, qh, N, p->tau);
+          k_x2<L, X2_ADJ><<<g2, NT, SM::XH, p->stream>>>(yin + fo * NN, nz * NN, nullptr, 0, p->V1, NL, pf,
+                                                         nz * nbx2, tb, qh, N, p->tau, nb);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
         }
         // ---- Y2 (batched): v = D_y^* V1[b]; G_j += conj(Aw[b]) v  (PS: Ut[b][j] = Hq_y^* FFT_y(conj(Aw) v));
