@@ -168,6 +168,17 @@ __device__ __forceinline__ void dft_reg(float2 *v) {
 #ifndef HOLO_DIT
 #define HOLO_DIT 1
 #endif
+// HOLO_TW8=1: each stage-twiddle row also holds the DIT level twiddles omega e^{-i pi/8},
+// omega e^{-i pi/4}, omega e^{-3 i pi/8}, omega^2 e^{-i pi/4} (fp64-generated, 64-byte rows), so the
+// 16 FP32 instructions that derive them per twiddled stage become two more L1-resident loads.
+// 0 (default): 32-byte rows (omega, omega^2, omega^4, omega^8), level twiddles derived in registers.
+// MEASURED SLOWER with 1 (tools/fftbench2.cu 35.65 vs 35.40 us per 4096^2 set at 512 threads, 35.03 vs
+// 32.06 at 2 x 256; cfg3 sweep 926.2 vs 947.7 frame-it/s, profiles/r02_tw8.log): the extra loads
+// cost more on the L1 / shared-memory path than the FP32 instructions they remove.
+#ifndef HOLO_TW8
+#define HOLO_TW8 0
+#endif
+constexpr int TW_ROW_F2 = HOLO_TW8 ? 8 : 4;  // float2 per twiddle row (the host builds the same rows)
 
 // (a, b) <- (a + t b, a - t b), runtime twiddle t
 __device__ __forceinline__ void bfly(float2 &a, float2 &b, float2 t) {
@@ -239,18 +250,15 @@ __device__ __forceinline__ void dft16_dit(float2 *v) {
   for (int i = 0; i < 16; i++) v[i] = a[i];
 }
 
-// twiddled 16-point step: y[k] = sum_s v[s] (omega W16^k)^s, given omega^{1,2,4,8} (forward
-// convention; INV uses the conjugates)
+// twiddled 16-point step: y[k] = sum_s v[s] (omega W16^k)^s, given omega^{1,2,4,8} and the level
+// twiddles t1 = omega e^{-i pi/8}, t2 = omega e^{-i pi/4}, t3 = omega e^{-3 i pi/8}, s1 = omega^2 e^{-i pi/4}
+// (forward convention; INV uses the conjugates)
 template <bool INV>
-__device__ __forceinline__ void dft16_dit_tw(float2 *v, float2 w1, float2 w2, float2 w4, float2 w8) {
-  constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f, H = 0.70710678118654752f;
+__device__ __forceinline__ void dft16_dit_tw8(float2 *v, float2 w1, float2 w2, float2 w4, float2 w8, float2 t1,
+                                              float2 t2, float2 t3, float2 s1) {
   auto mi = [](float2 z) { return make_float2(z.y, -z.x); };  // -i z
   auto cj = [](float2 z) { return INV ? make_float2(z.x, -z.y) : z; };
-  // level twiddles (forward convention), then conjugated for INV
-  const float2 t0 = w1, t1 = make_float2(fmaf(w1.x, C1, w1.y * S1), fmaf(w1.y, C1, -w1.x * S1)),
-               t2 = make_float2((w1.x + w1.y) * H, (w1.y - w1.x) * H),
-               t3 = make_float2(fmaf(w1.x, S1, w1.y * C1), fmaf(w1.y, S1, -w1.x * C1));
-  const float2 s0 = w2, s1 = make_float2((w2.x + w2.y) * H, (w2.y - w2.x) * H);
+  const float2 t0 = w1, s0 = w2;
   float2 a[16];
 #pragma unroll
   for (int i = 0; i < 16; i++) a[i] = v[brev4(i)];
@@ -287,6 +295,28 @@ __device__ __forceinline__ void dft16_dit_tw(float2 *v, float2 w1, float2 w2, fl
   bfly(a[7], a[15], cj(mi(t3)));
 #pragma unroll
   for (int i = 0; i < 16; i++) v[i] = a[i];
+}
+// the same with the level twiddles derived from omega in registers (HOLO_TW8 = 0)
+template <bool INV>
+__device__ __forceinline__ void dft16_dit_tw(float2 *v, float2 w1, float2 w2, float2 w4, float2 w8) {
+  constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f, H = 0.70710678118654752f;
+  const float2 t1 = make_float2(fmaf(w1.x, C1, w1.y * S1), fmaf(w1.y, C1, -w1.x * S1)),
+               t2 = make_float2((w1.x + w1.y) * H, (w1.y - w1.x) * H),
+               t3 = make_float2(fmaf(w1.x, S1, w1.y * C1), fmaf(w1.y, S1, -w1.x * C1));
+  const float2 s1 = make_float2((w2.x + w2.y) * H, (w2.y - w2.x) * H);
+  dft16_dit_tw8<INV>(v, w1, w2, w4, w8, t1, t2, t3, s1);
+}
+// one stage-twiddle row (TW_ROW_F2 float2) -> the twiddled 16-point step
+template <bool INV>
+__device__ __forceinline__ void dft16_row(float2 *v, const float4 *__restrict__ row) {
+  const float4 a = __ldg(row), b = __ldg(row + 1);
+#if HOLO_TW8
+  const float4 c = __ldg(row + 2), d = __ldg(row + 3);
+  dft16_dit_tw8<INV>(v, make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y), make_float2(b.z, b.w),
+                     make_float2(c.x, c.y), make_float2(c.z, c.w), make_float2(d.x, d.y), make_float2(d.z, d.w));
+#else
+  dft16_dit_tw<INV>(v, make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y), make_float2(b.z, b.w));
+#endif
 }
 
 template <int L>
@@ -354,10 +384,7 @@ __device__ __forceinline__ void r16_stage(float2 (&v)[16], Xch &x, const int t, 
   constexpr int ROW0 = S::F * (pow16(ST) - 1) / 15;
   const int m = t & (Ns - 1);
 #if HOLO_DIT
-  {
-    const float4 a = __ldg(tw + 2 * (ROW0 + m)), b = __ldg(tw + 2 * (ROW0 + m) + 1);
-    dft16_dit_tw<INV>(v, make_float2(a.x, a.y), make_float2(a.z, a.w), make_float2(b.x, b.y), make_float2(b.z, b.w));
-  }
+  dft16_row<INV>(v, tw + (TW_ROW_F2 / 2) * (ROW0 + m));
 #elif HOLO_TW_FULL
   {
     // full table: rows of 8 float4 = 16 float2 (entry 0 unused) per (stage, m)
@@ -371,7 +398,7 @@ __device__ __forceinline__ void r16_stage(float2 (&v)[16], Xch &x, const int t, 
   }
 #else
   {
-    const float4 a = __ldg(tw + 2 * (ROW0 + m)), b = __ldg(tw + 2 * (ROW0 + m) + 1);
+    const float4 a = __ldg(tw + (TW_ROW_F2 / 2) * (ROW0 + m)), b = __ldg(tw + (TW_ROW_F2 / 2) * (ROW0 + m) + 1);
     const float2 w1 = make_float2(a.x, a.y), w2 = make_float2(a.z, a.w), w4 = make_float2(b.x, b.y),
                  w8 = make_float2(b.z, b.w);
     twmul<INV>(v[1], w1);
@@ -473,11 +500,20 @@ __device__ __forceinline__ void r16_stage_nv(float2 (&v)[NV * 16], float2 *buf, 
   constexpr int ROW0 = S::F * (pow16(ST) - 1) / 15;
   const int m = t & (Ns - 1);
   {
-    const float4 a = __ldg(tw + 2 * (ROW0 + m)), b = __ldg(tw + 2 * (ROW0 + m) + 1);
+    const float4 *row = tw + (TW_ROW_F2 / 2) * (ROW0 + m);
+    const float4 a = __ldg(row), b = __ldg(row + 1);
     const float2 w1 = make_float2(a.x, a.y), w2 = make_float2(a.z, a.w), w4 = make_float2(b.x, b.y),
                  w8 = make_float2(b.z, b.w);
+#if HOLO_TW8
+    const float4 c = __ldg(row + 2), d = __ldg(row + 3);
+    const float2 t1 = make_float2(c.x, c.y), t2 = make_float2(c.z, c.w), t3 = make_float2(d.x, d.y),
+                 s1 = make_float2(d.z, d.w);
+#pragma unroll
+    for (int s = 0; s < NV; s++) dft16_dit_tw8<INV>(v + 16 * s, w1, w2, w4, w8, t1, t2, t3, s1);
+#else
 #pragma unroll
     for (int s = 0; s < NV; s++) dft16_dit_tw<INV>(v + 16 * s, w1, w2, w4, w8);
+#endif
   }
   if constexpr (ST + 1 < S::S16) {
     const int base = (t - m) * 16 + m;

@@ -271,7 +271,7 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   const int LT = chain_L(L) ? L : L / 3;  // line length of the Stockham engine (6144 = 3 x 2048)
   const int S16 = radix16_stages(LT), F = LT >> (4 * S16);
   const size_t twrows = (size_t)F * (((size_t)1 << (4 * S16)) - 1) / 15;  // F (16^S16 - 1) / 15
-  A(&p->tw, sizeof(float2) * 4 * twrows);
+  A(&p->tw, sizeof(float2) * holo::TW_ROW_F2 * twrows);
   A(&p->hdet, sizeof(float2) * L * nz);
   A(&p->homega, sizeof(float2) * L * nz);
   A(&p->cout, sizeof(float2) * L * nz);
@@ -304,12 +304,21 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   // ---- tables (fp64 -> fp32)
   {
     // FFT stage twiddle rows: radix-16 stage with Ns = F 16^st holds, per m < Ns,
-    // (w^m, w^2m, w^4m, w^8m), w = exp(-2 pi i / (16 Ns))   (fft_engine.cuh)
+    // (w^m, w^2m, w^4m, w^8m), w = exp(-2 pi i / (16 Ns)), and with HOLO_TW8 the DIT level twiddles
+    // w^m e^{-i pi/8}, w^m e^{-i pi/4}, w^m e^{-3 i pi/8}, w^2m e^{-i pi/4}   (fft_engine.cuh)
     std::vector<cd> tw;
     for (int Ns = F; Ns < LT; Ns *= 16)
-      for (int m = 0; m < Ns; m++)
+      for (int m = 0; m < Ns; m++) {
+        const double f = -(double)m / (16.0 * Ns);  // cycles of w^m
         for (int e : {1, 2, 4, 8}) tw.push_back(expi2pi_frac(-(double)((long)m * e) / (16.0 * Ns)));
-    if (tw.size() != 4 * twrows) { holo_plan_destroy(p); return HOLO_EUNSUPPORTED; }
+        if (holo::TW_ROW_F2 == 8) {
+          tw.push_back(expi2pi_frac(f - 1.0 / 16));
+          tw.push_back(expi2pi_frac(f - 1.0 / 8));
+          tw.push_back(expi2pi_frac(f - 3.0 / 16));
+          tw.push_back(expi2pi_frac(2 * f - 1.0 / 8));
+        }
+      }
+    if (tw.size() != (size_t)holo::TW_ROW_F2 * twrows) { holo_plan_destroy(p); return HOLO_EUNSUPPORTED; }
     if (s == HOLO_OK) s = upload(p, p->tw, tw);
     std::vector<cd> hd, ho, co, be, bo, pci, pco, pbe, pbo;
     p->cin_host.clear();

@@ -62,10 +62,17 @@ int main() {
   std::vector<float2> twh;
   for (int Ns = 16; Ns < L; Ns *= 16)
     for (int m = 0; m < Ns; m++)
+    {
       for (int e : {1, 2, 4, 8}) {
         double a = -2.0 * M_PI * (double)((long)m * e) / (16.0 * Ns);
         twh.push_back(make_float2((float)cos(a), (float)sin(a)));
       }
+      if (TW_ROW_F2 == 8) {  // DIT level twiddles (fft_engine.cuh, HOLO_TW8)
+        const double f = -2.0 * M_PI * (double)m / (16.0 * Ns);
+        for (double a : {f - M_PI / 8, f - M_PI / 4, f - 3 * M_PI / 8, 2 * f - M_PI / 4})
+          twh.push_back(make_float2((float)cos(a), (float)sin(a)));
+      }
+    }
   std::vector<float2> hh(2 * L), xin((size_t)L * L);
   for (int i = 0; i < 2 * L; i++) hh[i] = make_float2((float)cos(0.001 * i * i) / L, (float)sin(0.001 * i * i) / L);
   for (size_t i = 0; i < xin.size(); i++) xin[i] = make_float2((float)sin(0.37 * i), (float)cos(0.11 * i * 1.3));
