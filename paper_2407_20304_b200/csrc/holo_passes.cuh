@@ -56,6 +56,34 @@ __device__ __forceinline__ void st_p2_col(const float2 (&v)[16], float2 *__restr
   for (int r = 0; r < 16; r++) a[p2(t + r * (L / 16), x, R)] = v[r];
 }
 
+// Column staging (HOLO_STAGE, default 1).  A column pass's CTA owns G adjacent columns, i.e. ONE
+// contiguous block of 8 G L bytes of a P2 array (G/2 column pairs).  The frame's block is bulk-copied
+// (cp.async.bulk: the TMA engine, completion on an mbarrier) into the CTA's 64 KB thread-private
+// slot, where it also serves as the magnification's source and stash; the copy of frame b + 1 is
+// issued as soon as frame b's last access to the slot is behind a CTA barrier (the next transform's
+// exchange), so it lands while frame b's remaining transforms run.  It replaces the 16 LDG per
+// thread whose L2 latency every frame start exposed.  Element (y, col0 + g) of the block sits at
+// 2 L (g >> 1) + 2 y + (g & 1): a warp's (t, g) lanes read consecutive float2 (conflict free, G = 2).
+#ifndef HOLO_STAGE
+#define HOLO_STAGE 1
+#endif
+struct ColStage {
+  uint64_t *bar;       // the slot's mbarrier
+  const float2 *next;  // the next frame's block (nullptr: last frame)
+  uint32_t bytes;      // 8 G L
+  uint32_t phase;      // parity of this frame's copy
+  // all threads, after a CTA barrier that follows their last access to the slot
+  __device__ __forceinline__ void issue_next(float2 *slot) const {
+    if (next && threadIdx.x == 0) {
+      fence_proxy_async();  // the generic-proxy reads / writes of the slot precede the async write
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(slot, next, bytes, bar);
+    }
+  }
+};
+template <int L>
+__device__ __forceinline__ int stage_idx(int g, int y) { return 2 * L * (g >> 1) + 2 * y + (g & 1); }
+
 // ----------------------------------------------------------------------------- X1
 // rows of psi_k (row-major):  X = FFT(psi row) (kept thread-private); per j: T1_j row = M_{1/mt_j} S_{sx} psi row
 // (one non-inlined call per plane: only pointers and the pipe state cross it, so the
@@ -153,25 +181,38 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // PS (per-frame probe shifts): q_kj = P_omega S_{s^p} q is not a
 // per-plane constant; its column comes from qt = IDFT_x(Hq_x Qhat) (XQ pass, spectral in y):
 // x Hq_y (table), IFFT_y -> q_kj column, stored to qk (Y2 needs conj(q_kj)).
-template <int L, bool PS>
+template <int L, bool PS, bool STG>
 __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const float2 *__restrict__ qj,
                                       const float2 *__restrict__ qt, float2 *__restrict__ qk,
                                       float2 *__restrict__ aout, float2 *__restrict__ w1, const float4 *__restrict__ tw,
-                                      const TabSeq &seq, TabPipe<L> pipe, float2 *sm, int mag, int N, int fourier) {
+                                      const TabSeq &seq, TabPipe<L> pipe, float2 *sm, int mag, int N, int fourier,
+                                      ColStage st) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   Xch x = C::xch(sm);
   const Priv<NT> X{priv_base<L>(sm)};
+  float2 *Sb = priv_base<L>(sm);
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
+  const int s0 = stage_idx<L>(C::g(), t);
+  // the thread-private slot: the staged block (STG) or the Priv layout
+  auto slot = [&](int r) -> float2 & { if constexpr (STG) return Sb[s0 + 2 * r * T]; else return X[r]; };
   float2 v[16];
-  ld_p2_col<L>(v, in, col, L, t);
+  if constexpr (STG) {
+    mbar_wait(st.bar, st.phase);
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = slot(r);
+  } else {
+    ld_p2_col<L>(v, in, col, L, t);
+  }
   if (!fourier) fft<L, false>(v, x, t, tw);  // HOLO_FOURIER: T1 is already the y-spectrum (X1 ran on DFT2 psi)
   if (mag) {
+    if (!STG || !fourier) {  // (staged Fourier-state input: the slot already holds the spectrum)
 #pragma unroll
-    for (int r = 0; r < 16; r++) X[r] = v[r];
+      for (int r = 0; r < 16; r++) slot(r) = v[r];
+    }
     mag_fwd<L>(
-        v, [&](int r) { return X[r]; }, [&](int r, float2 e) { X[r] = e; }, [&](int r) { return X[r]; }, pipe, seq,
-        false, x, t, tw);
+        v, [&](int r) { return slot(r); }, [&](int r, float2 e) { slot(r) = e; }, [&](int r) { return slot(r); },
+        pipe, seq, false, x, t, tw);
   } else {
     const float2 *cr = pipe.take(seq);
 #pragma unroll
@@ -199,7 +240,9 @@ __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + p2(t + r * T, col, L)));
   }
   if (w1) {
+    if constexpr (STG) fence_proxy_async();  // this thread's slot accesses before the next async write
     fft<L, false>(v, x, t, tw);
+    if constexpr (STG) st.issue_next(Sb);  // every thread is past its last slot access (the FFT's barriers)
     const float2 *h = pipe.take(seq);  // hdet_j / L
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], h[t + r * T]);
@@ -211,6 +254,10 @@ __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const
       const int row = t + r * T - o;
       if (row >= 0 && row < N) w1[p2(row, col, N)] = v[r];
     }
+  } else if constexpr (STG) {
+    fence_proxy_async();
+    __syncthreads();
+    st.issue_next(Sb);
   }
   return pipe;
 }
@@ -221,20 +268,35 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
          float2 *__restrict__ Qk, float2 *__restrict__ Aout, float2 *__restrict__ W1, Tables tb,
          const __grid_constant__ TabSeq seq, int mag, int N, int nb, int fourier) {
   using C = CtaK<L>;
+  constexpr bool STG = HOLO_STAGE && !PS && C::G >= 2;
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
+  __shared__ uint64_t sbar;
   float2 *sm = reinterpret_cast<float2 *>(sm4);
+  const int col0 = blockIdx.x * C::G;
+  constexpr uint32_t SBYTES = 8u * C::G * L;
+  if (STG && threadIdx.x == 0) {
+    mbar_init(&sbar, 1);
+    fence_mbar_init();
+  }
   TabPipe<L> pipe;
   pipe.start(seq, slot_base<L, true>(sm), bars);
-  const int col0 = blockIdx.x * C::G;
+  if (STG) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&sbar, SBYTES);
+      bulk_g2s(priv_base<L>(sm), T1j + p2(0, col0, L), SBYTES, &sbar);
+    }
+  }
   constexpr int PF_COLS = C::G < 2 ? 2 : C::G;  // whole P2 column pairs (16-byte aligned blocks)
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *in = T1j + (size_t)b * fstride;
     if (threadIdx.x == 0 && b + 1 < nb) prefetch_l2(in + fstride + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
-    pipe = y1_frame<L, PS>(in, qj, PS ? Qt + (size_t)b * fstride : nullptr, (PS && Qk) ? Qk + (size_t)b * L * L : nullptr,
-                    Aout ? Aout + (size_t)b * L * L : nullptr, W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq, pipe,
-                    sm, mag, N, fourier);
+    const ColStage st{&sbar, b + 1 < nb ? in + fstride + p2(0, col0, L) : nullptr, SBYTES, (uint32_t)(b & 1)};
+    pipe = y1_frame<L, PS, STG>(in, qj, PS ? Qt + (size_t)b * fstride : nullptr,
+                                (PS && Qk) ? Qk + (size_t)b * L * L : nullptr, Aout ? Aout + (size_t)b * L * L : nullptr,
+                                W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq, pipe, sm, mag, N, fourier, st);
   }
 }
 
