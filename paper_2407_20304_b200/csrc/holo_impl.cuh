@@ -4,6 +4,7 @@
 // themselves (holo_run.cuh) are instantiated once per L in their own TU so that the
 // seven sizes compile in parallel.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <complex>
@@ -31,6 +32,9 @@ struct holo_plan {
   // workspace (P2 layout, holo_kernels.cuh):
   //   T1 [B][nz][L][L], Aw [B][L][L], W1 / V1 [B][N][L], T3 [B][nz][L][L], G [nz][L][L], QJ [nz][L][L]
   float2 *T1 = nullptr, *Aw = nullptr, *W1 = nullptr, *V1 = nullptr, *T3 = nullptr, *G = nullptr, *QJ = nullptr;
+  // TMA descriptor of T3 for X3's row staging (HOLO_STAGE): {4 floats, L rows, L/2 column pairs, B nz planes}
+  CUtensorMap t3map{};
+  bool t3map_ok = false;
   double *partF = nullptr, *partX3 = nullptr, *partQ = nullptr;
   int nbx2 = 0, nbx3 = 0;  // CTAs of one frame's X2 launch / one angle's X3 launch (partials per CTA)
   float tau = 1.f;         // penalty exponent of the current call (G_tau, App. A.3): 1 = F_1, 2 = F_2

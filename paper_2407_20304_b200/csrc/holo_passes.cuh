@@ -536,16 +536,66 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // partial[blk][0] = sum |g|^2, partial[blk][1] = sum Re(g conj(eta))   (g, eta row-major)
 // The sum over planes is kept in the g row itself (L2-resident between planes); each plane
 // is one non-inlined call (spill-free magnification).
-template <int L>
+// Row staging (HOLO_STAGE, X3): the CTA's G rows of plane j of T3 (P2: 2048 strided 32-byte pieces at
+// L = 4096) are gathered by 4-D tensor copies (TMA, tma.cuh) into the 64 KB thread-private slot; the
+// copy of plane j + 1 is issued as soon as the magnification's last source read is behind a CTA
+// barrier, so it lands while plane j's last two transforms run.  Element (y0 + g, x) of the staged
+// rows sits at 2 (G (x >> 1) + g) + (x & 1) (the box order {x & 1, g, x >> 1}): a warp's (t, g)
+// lanes read consecutive float2.
+struct RowStage {
+  const CUtensorMap *map;  // T3 as {4 floats, L rows, L/2 column pairs, planes}
+  uint64_t *bar;
+  int next;                // plane index (in the map) of the next copy, -1: none
+  int y0;
+  uint32_t phase;          // parity of this plane's copy
+  template <int L>
+  __device__ __forceinline__ void issue(float2 *slot, int plane) const {
+    using C = CtaK<L>;
+    constexpr int BOXC = L / 2 < 256 ? L / 2 : 256;  // column pairs per box
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, 8u * C::G * L);
+#pragma unroll 1
+      for (int c = 0; c < L / 2; c += BOXC) tma_load_4d(slot + 2 * C::G * c, map, 0, y0, c, plane, bar);
+    }
+  }
+};
+
+template <int L, bool STG>
 __device__ __noinline__ TabPipe<L> x3_plane(const float2 *__restrict__ T3j, float2 *__restrict__ grow,
                                       const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> pipe, float2 *sm,
-                                      bool mag, int j, bool last) {
+                                      bool mag, int j, bool last, RowStage rs, float2 *pv) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   Xch x = C::xch(sm);
-  const Priv<NT> Z{priv_base<L>(sm)};
+  const Priv<NT> Z{pv};  // the private slot, 128-byte aligned for the tensor copies (k_x3)
+  float2 *Zs = pv;
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 v[16];
+  if constexpr (STG) {
+    auto S = [&](int r) {
+      const int xx = t + r * T;
+      return Zs[2 * (C::G * (xx >> 1) + C::g()) + (xx & 1)];
+    };
+    auto freed = [&]() {
+      if (rs.next >= 0) rs.template issue<L>(Zs, rs.next);
+    };
+    mbar_wait(rs.bar, rs.phase);
+    if (mag) {
+      float2 e[16];
+      mag_adj<L>(
+          v, S, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe, seq, j > 0, x, t, tw,
+          freed);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = S(r);
+      fft<L, false>(v, x, t, tw);
+      freed();
+      const float2 *cr = pipe.take(seq);
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
+      pipe.done(seq);
+    }
+  } else {
 #if HOLO_X3_ZACC
   // the plane sum stays in the private slot Z; the magnification reads its source twice from
   // global memory (the second read hits L2)
@@ -592,6 +642,7 @@ __device__ __noinline__ TabPipe<L> x3_plane(const float2 *__restrict__ T3j, floa
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
     pipe.done(seq);
   }
+  }  // !STG
   // sum over planes in the g row (one owner thread per element): store, then fire-and-forget
   // adds, and the last plane reads the sum back (L2, __ldcg) into the private slot
   if (j == 0 && !last) {
@@ -611,23 +662,47 @@ template <int L>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x3(const float2 *__restrict__ T3, const float2 *__restrict__ eta, float2 *__restrict__ g,
          double *__restrict__ partial, Tables tb, const __grid_constant__ TabSeq seq, int nz, uint32_t magmask,
-         float scale, int fourier) {
+         float scale, int fourier, const __grid_constant__ CUtensorMap t3map, int pl0, int staged) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
+  constexpr bool STG_OK = HOLO_STAGE && !HOLO_X3_ZACC && C::G >= 2;
   extern __shared__ float4 sm4[];
   __shared__ double red[32];
   __shared__ uint64_t bars[2];
+  __shared__ uint64_t sbar;
   float2 *sm = reinterpret_cast<float2 *>(sm4);
+  const int y0 = blockIdx.x * C::G;
+  const bool stg = STG_OK && staged;
+  if (stg && threadIdx.x == 0) {
+    mbar_init(&sbar, 1);
+    fence_mbar_init();
+  }
+  // [exchange][<= 112 B pad][private slot, 128-byte aligned: TMA destination][table slots] (Smem::XPT3)
+  float2 *pv = priv_base<L>(sm);
+  pv += ((128u - (smem_u32(pv) & 127u)) & 127u) / sizeof(float2);
   TabPipe<L> pipe;
-  pipe.start(seq, slot_base<L, true>(sm), bars);
+  pipe.start(seq, pv + CtaK<L>::PRIV / sizeof(float2), bars);
+  if (stg) {
+    __syncthreads();
+    RowStage{&t3map, &sbar, -1, y0, 0}.template issue<L>(pv, pl0);
+  }
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
   float2 *grow = g + (size_t)y * L;  // also the Fourier-domain accumulator of sum_j W_j
   if (eta && threadIdx.x == 0) prefetch_l2(eta + (size_t)blockIdx.x * C::G * L, 8u * C::G * L);  // read at the end
+  if (STG_OK && stg) {
 #pragma unroll 1
-  for (int j = 0; j < nz; j++)
-    pipe = x3_plane<L>(T3 + (size_t)j * L * L, grow, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j, j + 1 == nz);
+    for (int j = 0; j < nz; j++)
+      pipe = x3_plane<L, STG_OK>(T3 + (size_t)j * L * L, grow, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j,
+                                 j + 1 == nz, RowStage{&t3map, &sbar, j + 1 < nz ? pl0 + j + 1 : -1, y0, (uint32_t)(j & 1)},
+                                 pv);
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < nz; j++)
+      pipe = x3_plane<L, false>(T3 + (size_t)j * L * L, grow, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j,
+                                j + 1 == nz, RowStage{}, pv);
+  }
   Xch x = C::xch(sm);
-  const Priv<NT> Z{priv_base<L>(sm)};
+  const Priv<NT> Z{pv};
   float2 v[16];
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = Z[r];

@@ -21,6 +21,7 @@ struct Smem {
   static constexpr size_t XT = X + TabPipe<L>::BYTES;                    // + two table slots
   static constexpr size_t XPT = X + CtaK<L>::PRIV + TabPipe<L>::BYTES;  // + one thread-private line
   static constexpr size_t XH = X + sizeof(float2) * L;                   // + X2's resident table
+  static constexpr size_t XPT3 = XPT + 128;                              // X3: private slot 128-byte aligned
 };
 
 template <int L>
@@ -46,7 +47,7 @@ void set_chain_attrs() {
   a((const void *)k_x2<L, X2_ADJ>, S::XH);
   a((const void *)k_y2<L, false>, S::XPT);
   a((const void *)k_y2<L, true>, S::XPT);
-  a((const void *)k_x3<L>, S::XPT);
+  a((const void *)k_x3<L>, S::XPT3);
   a((const void *)k_rows_filter<L, false, true, false>, S::X);
   a((const void *)k_rows_filter<L, true, false, false>, S::X);
   a((const void *)k_rows_filter<L, true, false, true>, S::X);
@@ -425,9 +426,10 @@ struct Run {
             q3.p[q3.n++] = crp(k, j, 0);
         }
         pbeg(p);
-        k_x3<L><<<L / G, NT, SM::XPT, p->stream>>>(p->T3 + (size_t)b * nz * LL, eta ? eta + (size_t)k * LL : nullptr,
+        k_x3<L><<<L / G, NT, SM::XPT3, p->stream>>>(p->T3 + (size_t)b * nz * LL, eta ? eta + (size_t)k * LL : nullptr,
                                                     gpsi + (size_t)k * LL, p->partX3 + (size_t)k * 2 * p->nbx3, tb, q3,
-                                                    nz, p->magmask, fo_ ? gscale * (float)L * (float)L : gscale, fo_);
+                                                    nz, p->magmask, fo_ ? gscale * (float)L * (float)L : gscale, fo_,
+                                                    p->t3map, b * nz, p->t3map_ok ? 1 : 0);
         pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + (fo_ ? 0 : 1)));
       };
       const bool want_x3 = gpsi && (mode == 0 || mode == 2);

@@ -1,8 +1,8 @@
 // tma.cuh -- minimal TMA (cp.async.bulk.tensor) + mbarrier helpers for sm_100a, raw PTX.
 //
-// Column passes stage a pair of columns of an L x L complex64 array through shared
-// memory with 2-D tensor copies (box = {2 complex, 256 rows}): the copy engine moves
-// the 16-byte row pieces, the LSU never sees the scattered sectors.
+// X3 stages the G rows of a P2 workspace plane that a CTA owns (2048 strided 32-byte pieces at
+// L = 4096) through shared memory with 4-D tensor copies (holo_passes.cuh, HOLO_STAGE): the copy
+// engine gathers the row pieces, the LSU never sees the scattered sectors.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -44,6 +44,15 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           smem_u32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// 4-D tensor load (c0 innermost), completion on an mbarrier
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, int c0, int c1, const void *src) {
