@@ -434,24 +434,61 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // PS: instead of G_j += conj(a) v, the frame's probe-gradient term u = conj(a) v is taken to
 // the y-spectrum with conj(Hq_y) and stored to ut (XG finishes the x axis and accumulates
 // the Fourier-domain sum, Eq. (12) with Q_kj^* = S_{-s^p} P_{-omega}); conj(q_kj) comes from qk.
-template <int L, bool PS>
+// Column staging in Y2 (HOLO_STAGE_Y2, default 1; non-PS launches with G >= 2): the CTA's V1 block
+// (8 G N bytes, contiguous in P2) and, when the probe gradient is accumulated, its block of a
+// (8 G L bytes) are bulk-copied (cp.async.bulk + mbarrier) through the thread-private slot instead
+// of 2 x 16 LDG per thread: V1 of frame b + 1 is issued once the magnification's last source read of
+// frame b is behind a barrier (mag_adj's src_freed hook; the first half's term is parked in
+// registers as in X3), a of frame b once the first transform's barriers are past the V1 reads, so
+// it lands behind D_y^*'s two transforms.  Copies complete alternating phases of one mbarrier.
+#ifndef HOLO_STAGE_Y2
+#define HOLO_STAGE_Y2 1
+#endif
+struct Y2Stage {
+  uint64_t *bar;
+  const float2 *ablk;   // this frame's block of a (nullptr: not staged)
+  const float2 *vnext;  // the next frame's V1 block (nullptr: last frame)
+  uint32_t vbytes, abytes;
+  uint32_t vphase;      // parity of this frame's V1 copy (its a copy, if any, completes parity 1)
+};
+
+template <int L, bool PS, bool STG>
 __device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, const float2 *__restrict__ ab,
                                       const float2 *__restrict__ qj, float2 *__restrict__ Gj, float2 *__restrict__ ut,
                                       float2 *__restrict__ t3, const float4 *__restrict__ tw, const TabSeq &seq,
-                                      TabPipe<L> pipe, float2 *sm, int mag, int N, int fourier) {
+                                      TabPipe<L> pipe, float2 *sm, int mag, int N, int fourier, Y2Stage st) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   Xch x = C::xch(sm);
   const Priv<NT> Y{priv_base<L>(sm)};
+  float2 *Sb = priv_base<L>(sm);
   const int t = C::t(), col = blockIdx.x * C::G + C::g();
   const int o = (L - N) / 2;
   float2 v[16];
+  if constexpr (STG) {
+    const int v0 = 2 * N * (C::g() >> 1) + (C::g() & 1);  // element (row, col) of the V1 block at v0 + 2 row
+    mbar_wait(st.bar, st.vphase);
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
-    const int row = t + r * T - o;
-    v[r] = (row >= 0 && row < N) ? ldg2(vin + p2(row, col, N)) : make_float2(0.f, 0.f);
+    for (int r = 0; r < 16; r++) {
+      const int row = t + r * T - o;
+      v[r] = (row >= 0 && row < N) ? Sb[v0 + 2 * row] : make_float2(0.f, 0.f);
+    }
+    fence_proxy_async();  // this thread's reads of the slot precede the async write of a
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const int row = t + r * T - o;
+      v[r] = (row >= 0 && row < N) ? ldg2(vin + p2(row, col, N)) : make_float2(0.f, 0.f);
+    }
   }
   fft<L, false>(v, x, t, tw);
+  if constexpr (STG) {
+    if (st.ablk && threadIdx.x == 0) {  // every thread is past its V1 reads (the transform's barriers)
+      fence_proxy_async();
+      mbar_expect_tx(st.bar, st.abytes);
+      bulk_g2s(Sb, st.ablk, st.abytes, st.bar);
+    }
+  }
   {
     const float2 *h = pipe.take(seq);  // hdet_j / L, conjugated
 #pragma unroll
@@ -459,6 +496,9 @@ __device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, cons
     pipe.done(seq);
   }
   fft<L, true>(v, x, t, tw);
+  const int s0 = stage_idx<L>(C::g(), t);
+  // the thread-private slot: the staged layout (STG; element (y, col) where the block of a has it) or Priv
+  auto slot = [&](int r) -> float2 & { if constexpr (STG) return Sb[s0 + 2 * r * T]; else return Y[r]; };
   if (PS && ut) {
 #pragma unroll
     for (int r = 0; r < 16; r++) {
@@ -474,23 +514,51 @@ __device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, cons
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = Y[r];
   } else if (Gj) {
+    if constexpr (STG) mbar_wait(st.bar, 1);
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const size_t gi = p2(t + r * T, col, L);
-      red_add2(Gj + gi, cmulc(v[r], ldg2(ab + gi)));  // G_j += conj(a) v (this thread owns gi)
+      float2 av;
+      if constexpr (STG) av = slot(r); else av = ldg2(ab + gi);
+      red_add2(Gj + gi, cmulc(v[r], av));  // G_j += conj(a) v (this thread owns gi)
     }
   }
-  if (!t3) return pipe;
+  auto issue_next = [&]() {  // all threads, behind a CTA barrier that follows their last slot access
+    if constexpr (STG) {
+      if (st.vnext && threadIdx.x == 0) {
+        fence_proxy_async();
+        mbar_expect_tx(st.bar, st.vbytes);
+        bulk_g2s(Sb, st.vnext, st.vbytes, st.bar);
+      }
+    }
+  };
+  if (!t3) {
+    if constexpr (STG) {
+      fence_proxy_async();
+      __syncthreads();
+      issue_next();
+    }
+    return pipe;
+  }
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));  // qj: q_j, or q_kj (PS)
   if (mag) {
 #pragma unroll
-    for (int r = 0; r < 16; r++) Y[r] = v[r];
-    mag_adj<L>(
-        v, [&](int r) { return Y[r]; }, [&](int r, float2 e) { Y[r] = e; }, [&](int r) { return Y[r]; }, pipe, seq,
-        true, x, t, tw);
+    for (int r = 0; r < 16; r++) slot(r) = v[r];
+    if constexpr (STG) {
+      float2 e[16];
+      mag_adj<L>(
+          v, [&](int r) { const float2 z = slot(r); if (r == 15) fence_proxy_async(); return z; },
+          [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe, seq, true, x, t, tw, issue_next);
+    } else {
+      mag_adj<L>(
+          v, [&](int r) { return Y[r]; }, [&](int r, float2 e) { Y[r] = e; }, [&](int r) { return Y[r]; }, pipe, seq,
+          true, x, t, tw);
+    }
   } else {
+    if constexpr (STG) fence_proxy_async();
     fft<L, false>(v, x, t, tw);
+    issue_next();
     const float2 *cr = pipe.take(seq);
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
@@ -507,14 +575,28 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
          const float2 *__restrict__ Qk, float2 *__restrict__ Gj, float2 *__restrict__ Ut, float2 *__restrict__ T3j,
          size_t fstride, Tables tb, const __grid_constant__ TabSeq seq, int mag, int N, int nb, int fourier) {
   using C = CtaK<L>;
+  constexpr bool STG = HOLO_STAGE && HOLO_STAGE_Y2 && !PS && C::G >= 2;
   extern __shared__ float4 sm4[];
   __shared__ uint64_t bars[2];
+  __shared__ uint64_t sbar;
   float2 *sm = reinterpret_cast<float2 *>(sm4);
+  if (STG && threadIdx.x == 0) {
+    mbar_init(&sbar, 1);
+    fence_mbar_init();
+  }
   TabPipe<L> pipe;
   pipe.start(seq, slot_base<L, true>(sm), bars);
   const int col0 = blockIdx.x * C::G;
   constexpr int PF_COLS = C::G < 2 ? 2 : C::G;  // whole P2 column pairs (16-byte aligned blocks)
   const bool wq = PS ? Ut != nullptr : Gj != nullptr;
+  const uint32_t VBYTES = 8u * C::G * N, ABYTES = 8u * C::G * L;
+  if (STG) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&sbar, VBYTES);
+      bulk_g2s(priv_base<L>(sm), V1 + p2(0, col0, N), VBYTES, &sbar);
+    }
+  }
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *vin = V1 + (size_t)b * N * L;
@@ -523,8 +605,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       prefetch_l2(vin + (size_t)N * L + p2(0, col0 & ~1, N), 8u * PF_COLS * N);
       if (wq) prefetch_l2(ab + (size_t)L * L + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
     }
-    pipe = y2_frame<L, PS>(vin, ab, PS ? Qk + (size_t)b * L * L : qj, Gj, (PS && Ut) ? Ut + (size_t)b * fstride : nullptr,
-                    T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N, fourier);
+    const Y2Stage st{&sbar, wq ? ab + p2(0, col0, L) : nullptr, b + 1 < nb ? vin + (size_t)N * L + p2(0, col0, N) : nullptr,
+                     VBYTES, ABYTES, wq ? 0u : (uint32_t)(b & 1)};
+    pipe = y2_frame<L, PS, STG>(vin, ab, PS ? Qk + (size_t)b * L * L : qj, Gj, (PS && Ut) ? Ut + (size_t)b * fstride : nullptr,
+                    T3j ? T3j + (size_t)b * fstride : nullptr, tb.tw, seq, pipe, sm, mag, N, fourier, st);
   }
 }
 
