@@ -284,9 +284,15 @@ __device__ __forceinline__ float2 wodd_q(float2 base) {
 // SRC(r) is read before STASH(r, .) for the same r, so source and stash may share a
 // thread-private slot: only one line is live across each transform.  w is computed on
 // the fly; the pipe supplies, in order: cr, bke, cr, bko, cout.  v receives y.
-template <int L, class Src, class Stash, class Unstash>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+// SRC_FREED() runs after the transform that follows the last SRC read (its barriers: every thread of
+// the CTA is past its SRC reads), e.g. to reuse the source's shared memory.
+template <int L, class Src, class Stash, class Unstash, class Freed = NoHook>
 __device__ __forceinline__ void mag_fwd(float2 (&v)[16], Src src, Stash stash, Unstash unstash, TabPipe<L> &pipe,
-                                        const TabSeq &q, bool sync0, Xch &x, int t, const float4 *__restrict__ tw) {
+                                        const TabSeq &q, bool sync0, Xch &x, int t, const float4 *__restrict__ tw,
+                                        Freed src_freed = {}) {
   constexpr int T = L / 16;
   const float2 *tab = pipe.take(q, sync0);  // cr
 #pragma unroll
@@ -312,6 +318,7 @@ __device__ __forceinline__ void mag_fwd(float2 (&v)[16], Src src, Stash stash, U
 #undef HOLO_B
   pipe.done(q);
   fft<L, false>(v, x, t, tw);
+  src_freed();
   tab = pipe.take(q);  // bko
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = cmul(v[r], tab[t + r * T]);
@@ -331,11 +338,6 @@ __device__ __forceinline__ void mag_fwd(float2 (&v)[16], Src src, Stash stash, U
 // SRC(r): spatial input y at register r; STASH / UNSTASH as in mag_fwd.  The pipe
 // supplies, in order: cout, bke, cout, bko, cr.  v receives the SPECTRUM W (natural
 // order); the caller finishes with an inverse FFT (possibly after summing several W).
-struct NoHook {
-  __device__ __forceinline__ void operator()() const {}
-};
-// SRC_FREED() runs after the transform that follows the last SRC read (its barriers: every thread of
-// the CTA is past its SRC reads), e.g. to reuse the source's shared memory.
 template <int L, class Src, class Stash, class Unstash, class Freed = NoHook>
 __device__ __forceinline__ void mag_adj(float2 (&v)[16], Src src, Stash stash, Unstash unstash, TabPipe<L> &pipe,
                                         const TabSeq &q, bool sync0, Xch &x, int t, const float4 *__restrict__ tw,

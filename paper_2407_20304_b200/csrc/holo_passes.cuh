@@ -67,11 +67,16 @@ __device__ __forceinline__ void st_p2_col(const float2 (&v)[16], float2 *__restr
 #ifndef HOLO_STAGE
 #define HOLO_STAGE 1
 #endif
+#ifndef HOLO_STAGE_Q
+#define HOLO_STAGE_Q 1  // Y1: the q_j block through the slot too (bulk copy behind the magnification)
+#endif
 struct ColStage {
   uint64_t *bar;       // the slot's mbarrier
   const float2 *next;  // the next frame's block (nullptr: last frame)
   uint32_t bytes;      // 8 G L
   uint32_t phase;      // parity of this frame's copy
+  const float2 *qblk;  // Y1: the CTA's block of q_j, staged behind the magnification (nullptr: read by LDG);
+                       // its copy completes parity 1 (then the frame copies complete parity 0)
   // all threads, after a CTA barrier that follows their last access to the slot
   __device__ __forceinline__ void issue_next(float2 *slot) const {
     if (next && threadIdx.x == 0) {
@@ -210,9 +215,24 @@ __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const
 #pragma unroll
       for (int r = 0; r < 16; r++) slot(r) = v[r];
     }
-    mag_fwd<L>(
-        v, [&](int r) { return slot(r); }, [&](int r, float2 e) { slot(r) = e; }, [&](int r) { return slot(r); },
-        pipe, seq, false, x, t, tw);
+    if constexpr (STG) {
+      // the first half's term stays in registers (as in X1), so the slot is free once the second source
+      // read is behind a barrier: the q_j block lands there while the last two transforms run
+      float2 e[16];
+      mag_fwd<L>(
+          v, [&](int r) { const float2 z = slot(r); if (r == 15) fence_proxy_async(); return z; },
+          [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe, seq, false, x, t, tw, [&]() {
+            if (st.qblk && threadIdx.x == 0) {
+              fence_proxy_async();
+              mbar_expect_tx(st.bar, st.bytes);
+              bulk_g2s(Sb, st.qblk, st.bytes, st.bar);
+            }
+          });
+    } else {
+      mag_fwd<L>(
+          v, [&](int r) { return slot(r); }, [&](int r, float2 e) { slot(r) = e; }, [&](int r) { return slot(r); },
+          pipe, seq, false, x, t, tw);
+    }
   } else {
     const float2 *cr = pipe.take(seq);
 #pragma unroll
@@ -236,8 +256,14 @@ __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const
       for (int r = 0; r < 16; r++) v[r] = cmul(v[r], X[r]);
     }
   } else if (w1) {
+    if (STG && mag && st.qblk) {
+      mbar_wait(st.bar, 1);
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + p2(t + r * T, col, L)));
+      for (int r = 0; r < 16; r++) v[r] = cmul(v[r], slot(r));
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cmul(v[r], ldg2(qj + p2(t + r * T, col, L)));
+    }
   }
   if (w1) {
     if constexpr (STG) fence_proxy_async();  // this thread's slot accesses before the next async write
@@ -289,11 +315,13 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
   }
   constexpr int PF_COLS = C::G < 2 ? 2 : C::G;  // whole P2 column pairs (16-byte aligned blocks)
+  const bool qstg = STG && HOLO_STAGE_Q && mag && W1 && qj;  // q_j staged behind the magnification
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *in = T1j + (size_t)b * fstride;
     if (threadIdx.x == 0 && b + 1 < nb) prefetch_l2(in + fstride + p2(0, col0 & ~1, L), 8u * PF_COLS * L);
-    const ColStage st{&sbar, b + 1 < nb ? in + fstride + p2(0, col0, L) : nullptr, SBYTES, (uint32_t)(b & 1)};
+    const ColStage st{&sbar, b + 1 < nb ? in + fstride + p2(0, col0, L) : nullptr, SBYTES, qstg ? 0u : (uint32_t)(b & 1),
+                      qstg ? qj + p2(0, col0, L) : nullptr};
     pipe = y1_frame<L, PS, STG>(in, qj, PS ? Qt + (size_t)b * fstride : nullptr,
                                 (PS && Qk) ? Qk + (size_t)b * L * L : nullptr, Aout ? Aout + (size_t)b * L * L : nullptr,
                                 W1 ? W1 + (size_t)b * N * L : nullptr, tb.tw, seq, pipe, sm, mag, N, fourier, st);
