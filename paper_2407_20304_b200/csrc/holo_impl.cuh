@@ -33,8 +33,8 @@ struct holo_plan {
   //   T1 [B][nz][L][L], Aw [B][L][L], W1 / V1 [B][N][L], T3 [B][nz][L][L], G [nz][L][L], QJ [nz][L][L]
   float2 *T1 = nullptr, *Aw = nullptr, *W1 = nullptr, *V1 = nullptr, *T3 = nullptr, *G = nullptr, *QJ = nullptr;
   // TMA descriptor of T3 for X3's row staging (HOLO_STAGE): {4 floats, L rows, L/2 column pairs, B nz planes}
-  CUtensorMap t3map{};
-  bool t3map_ok = false;
+  CUtensorMap t3map{}, w1map{};
+  bool t3map_ok = false, w1map_ok = false;
   double *partF = nullptr, *partX3 = nullptr, *partQ = nullptr;
   int nbx2 = 0, nbx3 = 0;  // CTAs of one frame's X2 launch / one angle's X3 launch (partials per CTA)
   float tau = 1.f;         // penalty exponent of the current call (G_tau, App. A.3): 1 = F_1, 2 = F_2

@@ -328,6 +328,30 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   }
 }
 
+// Row staging (HOLO_STAGE, X3): the CTA's G rows of plane j of T3 (P2: 2048 strided 32-byte pieces at
+// L = 4096) are gathered by 4-D tensor copies (TMA, tma.cuh) into the 64 KB thread-private slot; the
+// copy of plane j + 1 is issued as soon as the magnification's last source read is behind a CTA
+// barrier, so it lands while plane j's last two transforms run.  Element (y0 + g, x) of the staged
+// rows sits at 2 (G (x >> 1) + g) + (x & 1) (the box order {x & 1, g, x >> 1}): a warp's (t, g)
+// lanes read consecutive float2.
+struct RowStage {
+  const CUtensorMap *map;  // T3 as {4 floats, L rows, L/2 column pairs, planes}
+  uint64_t *bar;
+  int next;                // plane index (in the map) of the next copy, -1: none
+  int y0;
+  uint32_t phase;          // parity of this plane's copy
+  template <int L>
+  __device__ __forceinline__ void issue(float2 *slot, int plane) const {
+    using C = CtaK<L>;
+    constexpr int BOXC = L / 2 < 256 ? L / 2 : 256;  // column pairs per box
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(bar, 8u * C::G * L);
+#pragma unroll 1
+      for (int c = 0; c < L / 2; c += BOXC) tma_load_4d(slot + 2 * C::G * c, map, 0, y0, c, plane, bar);
+    }
+  }
+};
+
 // ----------------------------------------------------------------------------- X2
 // rows y < N of the nb frames of a batch (one plane, so one transfer table for all of them).
 //   GRAD: W1 row -> D_x, crop, residual (+F), pad, D_x^* -> V1   (W1, V1: P2, N rows)
@@ -343,11 +367,19 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 #ifndef HOLO_X2_LOOP
 #define HOLO_X2_LOOP 1
 #endif
+// Row staging in X2 (HOLO_STAGE_X2, default 1; W1-reading modes with the frame loop): the CTA's G rows
+// of the frame's W1 (P2 with N rows: strided 32-byte pieces) are gathered by 4-D tensor copies into a
+// 64 KB slot, as X3 does for T3; the copy of frame b + 1 is issued once frame b's first transform is
+// past its barriers, so it lands behind the frame's four transforms.  Rows >= N read as zeros (the
+// tensor map's out-of-bounds fill).
+#ifndef HOLO_STAGE_X2
+#define HOLO_STAGE_X2 1
+#endif
 template <int L, int MODE, int TM>
 __device__ __forceinline__ void x2_frame(const float2 *__restrict__ in, const float *__restrict__ sqrt_d,
                                          float2 *__restrict__ out, double *__restrict__ partial, const float2 *h,
                                          Xch &x, const float4 *__restrict__ tw, double *red, int N, float tau,
-                                         uint64_t *bar) {
+                                         uint64_t *bar, const float2 *zs, RowStage rs) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
@@ -363,9 +395,20 @@ __device__ __forceinline__ void x2_frame(const float2 *__restrict__ in, const fl
     }
   }
   if (MODE != X2_ADJ) {
+    if (zs) {
+      mbar_wait(rs.bar, rs.phase);
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = act ? ldg2(in + p2(y, t + r * T, N)) : make_float2(0.f, 0.f);
-    fft<L, false>(v, x, t, tw);
+      for (int r = 0; r < 16; r++) {
+        const int xx = t + r * T;
+        v[r] = zs[2 * (C::G * (xx >> 1) + C::g()) + (xx & 1)];
+      }
+      fft<L, false>(v, x, t, tw);
+      if (rs.next >= 0) rs.template issue<L>(const_cast<float2 *>(zs), rs.next);  // every thread is past its slot reads
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = act ? ldg2(in + p2(y, t + r * T, N)) : make_float2(0.f, 0.f);
+      fft<L, false>(v, x, t, tw);
+    }
     mbar_wait(bar, 0);  // the resident table has arrived (returns at once after the first frame)
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], h[t + r * T]);
@@ -412,34 +455,43 @@ template <int L, int MODE, int TM = -1>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_x2(const float2 *__restrict__ in, size_t in_stride, const float *__restrict__ sqrt_d, size_t d_stride,
          float2 *__restrict__ out, size_t out_stride, double *__restrict__ partial, int part_stride, Tables tb,
-         const __grid_constant__ TabSeq seq, int N, float tau, int nb) {
+         const __grid_constant__ TabSeq seq, int N, float tau, int nb, const __grid_constant__ CUtensorMap w1map,
+         int staged) {
   using C = CtaK<L>;
   constexpr int T = L / 16;
+  constexpr bool STG_OK = HOLO_STAGE && HOLO_STAGE_X2 && HOLO_X2_LOOP && MODE != X2_ADJ && C::G >= 2;
   extern __shared__ float4 sm4[];
   __shared__ double red[32];
   __shared__ uint64_t bars[2];
+  __shared__ uint64_t sbar;
   float2 *sm = reinterpret_cast<float2 *>(sm4);
   Xch x = C::xch(sm);
   // the launch's only table (hdet_j / L; seq.p[0]) into the first slot, once
   float2 *h = slot_base<L, false>(sm);
+  const bool stg = STG_OK && staged;
+  // [exchange][table][<= 112 B pad][row slot, 128-byte aligned: TMA destination] (Smem::XHS)
+  float2 *zs = h + L;
+  zs += ((128u - (smem_u32(zs) & 127u)) & 127u) / sizeof(float2);
   if (threadIdx.x == 0) {
     mbar_init(bars, 1);
+    if (stg) mbar_init(&sbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
+  const int t = C::t(), y0 = blockIdx.x * C::G;
+  const int f0 = HOLO_X2_LOOP ? 0 : blockIdx.y, f1 = HOLO_X2_LOOP ? nb : blockIdx.y + 1;
+  if (stg) RowStage{&w1map, &sbar, -1, y0, 0}.template issue<L>(zs, f0);
   if (threadIdx.x == 0) {
     mbar_expect_tx(bars, L * sizeof(float2));
     bulk_g2s(h, seq.p[0], L * sizeof(float2), bars);
   }
-  const int t = C::t(), y0 = blockIdx.x * C::G;
-  const int f0 = HOLO_X2_LOOP ? 0 : blockIdx.y, f1 = HOLO_X2_LOOP ? nb : blockIdx.y + 1;
 #pragma unroll 1
   for (int fb = f0; fb < f1; fb++) {
     if (HOLO_X2_LOOP && fb + 1 < f1) {  // the next frame's rows into L2 (one lane per 32-byte sector)
       if (MODE == X2_ADJ) {
         if (threadIdx.x == 0 && y0 < N)
           prefetch_l2_any(in + (fb + 1) * in_stride + (size_t)y0 * N, 8u * N * (y0 + C::G <= N ? C::G : N - y0));
-      } else if ((threadIdx.x & 3) == 0 && y0 + C::g() < N) {
+      } else if (!stg && (threadIdx.x & 3) == 0 && y0 + C::g() < N) {
         const float2 *nx = in + (fb + 1) * in_stride;
 #pragma unroll
         for (int r = 0; r < 16; r++) prefetch_l2_sector(nx + p2(y0 + C::g(), t + r * T, N));
@@ -449,7 +501,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
     x2_frame<L, MODE, TM>(in + fb * in_stride, sqrt_d ? sqrt_d + fb * d_stride : nullptr,
                           out ? out + fb * out_stride : nullptr, partial + (size_t)fb * part_stride, h, x, tb.tw, red,
-                          N, tau, bars);
+                          N, tau, bars, stg ? zs : nullptr,
+                          RowStage{&w1map, &sbar, fb + 1 < f1 ? fb + 1 : -1, y0, (uint32_t)((fb - f0) & 1)});
   }
 }
 
@@ -471,6 +524,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 // it lands behind D_y^*'s two transforms.  Copies complete alternating phases of one mbarrier.
 #ifndef HOLO_STAGE_Y2
 #define HOLO_STAGE_Y2 1
+#endif
+#ifndef HOLO_Y2_QEARLY
+#define HOLO_Y2_QEARLY 0  // 1: q_j into registers before the wait for the block of a (spills: Y2 249 -> 271 us/frame); 2: L1 prefetch (252); 0: off
 #endif
 struct Y2Stage {
   uint64_t *bar;
@@ -527,6 +583,8 @@ __device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, cons
   const int s0 = stage_idx<L>(C::g(), t);
   // the thread-private slot: the staged layout (STG; element (y, col) where the block of a has it) or Priv
   auto slot = [&](int r) -> float2 & { if constexpr (STG) return Sb[s0 + 2 * r * T]; else return Y[r]; };
+  float2 qv[16];
+  bool qearly = false;
   if (PS && ut) {
 #pragma unroll
     for (int r = 0; r < 16; r++) {
@@ -542,6 +600,21 @@ __device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, cons
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = Y[r];
   } else if (Gj) {
+    if constexpr (STG && HOLO_Y2_QEARLY == 2) {
+      if (t3) {  // q_j's sectors into L1 while the block of a is awaited and G_j updated
+#pragma unroll
+        for (int r = 0; r < 16; r++)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(qj + p2(t + r * T, col, L)) : "memory");
+      }
+    }
+    if constexpr (STG && HOLO_Y2_QEARLY == 1) {
+      // q_j's L2 round trip overlaps the wait for the block of a and the G_j updates
+      if (t3) {
+#pragma unroll
+        for (int r = 0; r < 16; r++) qv[r] = ldg2(qj + p2(t + r * T, col, L));
+        qearly = true;
+      }
+    }
     if constexpr (STG) mbar_wait(st.bar, 1);
 #pragma unroll
     for (int r = 0; r < 16; r++) {
@@ -568,8 +641,13 @@ __device__ __noinline__ TabPipe<L> y2_frame(const float2 *__restrict__ vin, cons
     }
     return pipe;
   }
+  if (qearly) {
 #pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));  // qj: q_j, or q_kj (PS)
+    for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], qv[r]);
+  } else {
+#pragma unroll
+    for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], ldg2(qj + p2(t + r * T, col, L)));  // qj: q_j, or q_kj (PS)
+  }
   if (mag) {
 #pragma unroll
     for (int r = 0; r < 16; r++) slot(r) = v[r];
@@ -641,37 +719,20 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 }
 
 // ----------------------------------------------------------------------------- X3
+#ifndef HOLO_X3_TAIL
+#define HOLO_X3_TAIL 1  // the earlier planes' sum is read back in the kernel tail, together with eta
+#endif
 #ifndef HOLO_X3_ZACC
 #define HOLO_X3_ZACC 0  // 1: plane sum in the private slot, source read twice from global (L2)
+#endif
+#if HOLO_X3_ZACC
+#undef HOLO_X3_TAIL
+#define HOLO_X3_TAIL 0
 #endif
 // rows: g_k row = scale * IFFT( sum_j W_j ),  W_j = spectrum of (M S)_x^* T3_j row;
 // partial[blk][0] = sum |g|^2, partial[blk][1] = sum Re(g conj(eta))   (g, eta row-major)
 // The sum over planes is kept in the g row itself (L2-resident between planes); each plane
 // is one non-inlined call (spill-free magnification).
-// Row staging (HOLO_STAGE, X3): the CTA's G rows of plane j of T3 (P2: 2048 strided 32-byte pieces at
-// L = 4096) are gathered by 4-D tensor copies (TMA, tma.cuh) into the 64 KB thread-private slot; the
-// copy of plane j + 1 is issued as soon as the magnification's last source read is behind a CTA
-// barrier, so it lands while plane j's last two transforms run.  Element (y0 + g, x) of the staged
-// rows sits at 2 (G (x >> 1) + g) + (x & 1) (the box order {x & 1, g, x >> 1}): a warp's (t, g)
-// lanes read consecutive float2.
-struct RowStage {
-  const CUtensorMap *map;  // T3 as {4 floats, L rows, L/2 column pairs, planes}
-  uint64_t *bar;
-  int next;                // plane index (in the map) of the next copy, -1: none
-  int y0;
-  uint32_t phase;          // parity of this plane's copy
-  template <int L>
-  __device__ __forceinline__ void issue(float2 *slot, int plane) const {
-    using C = CtaK<L>;
-    constexpr int BOXC = L / 2 < 256 ? L / 2 : 256;  // column pairs per box
-    if (threadIdx.x == 0) {
-      mbar_expect_tx(bar, 8u * C::G * L);
-#pragma unroll 1
-      for (int c = 0; c < L / 2; c += BOXC) tma_load_4d(slot + 2 * C::G * c, map, 0, y0, c, plane, bar);
-    }
-  }
-};
-
 template <int L, bool STG>
 __device__ __noinline__ TabPipe<L> x3_plane(const float2 *__restrict__ T3j, float2 *__restrict__ grow,
                                       const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> pipe, float2 *sm,
@@ -764,8 +825,15 @@ __device__ __noinline__ TabPipe<L> x3_plane(const float2 *__restrict__ T3j, floa
 #pragma unroll
     for (int r = 0; r < 16; r++) red_add2(grow + t + r * T, v[r]);
   } else {
+#if HOLO_X3_TAIL
+    // the last plane's term goes to the kernel tail through the slot; the tail adds the L2-resident
+    // sum of the earlier planes (one round trip together with its eta reads)
+#pragma unroll
+    for (int r = 0; r < 16; r++) Z[r] = v[r];
+#else
 #pragma unroll
     for (int r = 0; r < 16; r++) Z[r] = j > 0 ? cadd(__ldcg(grow + t + r * T), v[r]) : v[r];
+#endif
   }
   return pipe;
 }
@@ -816,8 +884,38 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   Xch x = C::xch(sm);
   const Priv<NT> Z{pv};
   float2 v[16];
+#if HOLO_X3_TAIL
+  if (fourier && eta) {
+    // no transform in the tail: the plane sum and eta are fetched together
+    double gg = 0.0, ge = 0.0;
+    float2 sv[16], ev[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      sv[r] = nz > 1 ? __ldcg(grow + t + r * T) : make_float2(0.f, 0.f);
+      ev[r] = ldg2(eta + (size_t)y * L + t + r * T);
+    }
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const float2 a = cscale(cadd(sv[r], Z[r]), scale);
+      grow[t + r * T] = a;
+      gg += (double)(a.x * a.x + a.y * a.y);
+      ge += (double)(a.x * ev[r].x + a.y * ev[r].y);
+    }
+    const double s0 = block_sum(gg, red);
+    const double s1 = block_sum(ge, red);
+    if (threadIdx.x == 0) {
+      const double ps = 1.0 / ((double)L * L);
+      partial[2 * blockIdx.x] = s0 * ps;
+      partial[2 * blockIdx.x + 1] = s1 * ps;
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = nz > 1 ? cadd(__ldcg(grow + t + r * T), Z[r]) : Z[r];
+#else
 #pragma unroll
   for (int r = 0; r < 16; r++) v[r] = Z[r];
+#endif
   // HOLO_FOURIER: the rows are y-spectral (T3 from Y2) and the x-spectrum is kept: g = DFT2(grad) / L^2
   // before the caller's scale (2 L^2), and the dots carry Parseval's 1/L^2
   if (!fourier) fft<L, true>(v, x, t, tb.tw);

@@ -224,11 +224,11 @@ void holo_cg_flush(holo_plan *p) {
 
 extern "C" {
 
-// TMA descriptor of the T3 workspace for X3's row staging (holo_passes.cuh RowStage): the P2 plane as
-// a 4-D fp32 tensor {4 floats = one column pair of one row, L rows, L/2 column pairs, planes}, box
+// TMA descriptor of a P2 workspace (T3 for X3's row staging, W1 for X2's; holo_passes.cuh RowStage): the
+// P2 plane as a 4-D fp32 tensor {4 floats = one column pair of one row, R rows, L/2 column pairs, planes}, box
 // {4, G, min(256, L/2), 1}.  The encoder comes from the driver through the runtime (no -lcuda link).
 // false (X3 then loads its rows with LDG) if the driver entry point or the encoding is unavailable.
-static bool make_t3map(holo_plan *p, int planes) {
+static bool make_p2map(CUtensorMap *map, void *base, int L, int R, int planes) {
   typedef CUresult (*EncodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -239,13 +239,13 @@ static bool make_t3map(holo_plan *p, int planes) {
     cudaGetLastError();
     return false;
   }
-  const int L = p->L, G = 8192 / L;  // lines per 512-thread CTA (holo_kernels.cuh Cta)
+  const int G = 8192 / L;  // lines per 512-thread CTA (holo_kernels.cuh Cta)
   if (G < 2 || G > 256) return false;
-  const cuuint64_t dims[4] = {4, (cuuint64_t)L, (cuuint64_t)L / 2, (cuuint64_t)planes};
-  const cuuint64_t strides[3] = {16, 16ull * L, 8ull * L * L};  // bytes, dims 1..3
+  const cuuint64_t dims[4] = {4, (cuuint64_t)R, (cuuint64_t)L / 2, (cuuint64_t)planes};
+  const cuuint64_t strides[3] = {16, 16ull * R, 8ull * R * L};  // bytes, dims 1..3
   const cuuint32_t box[4] = {4, (cuuint32_t)G, (cuuint32_t)(L / 2 < 256 ? L / 2 : 256), 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = reinterpret_cast<EncodeTiled>(fn)(&p->t3map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, p->T3, dims, strides,
+  const CUresult r = reinterpret_cast<EncodeTiled>(fn)(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides,
                                                       box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -314,7 +314,10 @@ holo_status holo_plan_create(holo_plan **out, const holo_geometry *g, int device
   A(&p->T3, sizeof(float2) * LLc * nz * Bc);
   A(&p->G, sizeof(float2) * LLc * nz);
   A(&p->QJ, sizeof(float2) * LLc * nz);
-  if (s == HOLO_OK && p->T3 && chain_L(L)) p->t3map_ok = make_t3map(p, nz * (int)Bc);
+  if (s == HOLO_OK && p->T3 && chain_L(L)) {
+    p->t3map_ok = make_p2map(&p->t3map, p->T3, L, L, nz * (int)Bc);
+    p->w1map_ok = make_p2map(&p->w1map, p->W1, L, N, (int)Bc);  // X2's row staging (rows >= N read as zeros)
+  }
   A(&p->partF, sizeof(double) * Kc * nz * p->nbx2);
   A(&p->partX3, sizeof(double) * Kc * 2 * p->nbx3);
   A(&p->partQ, sizeof(double) * 2 * 1184);

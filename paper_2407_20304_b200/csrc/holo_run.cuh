@@ -22,6 +22,7 @@ struct Smem {
   static constexpr size_t XPT = X + CtaK<L>::PRIV + TabPipe<L>::BYTES;  // + one thread-private line
   static constexpr size_t XH = X + sizeof(float2) * L;                   // + X2's resident table
   static constexpr size_t XPT3 = XPT + 128;                              // X3: private slot 128-byte aligned
+  static constexpr size_t XHS = XH + 128 + CtaK<L>::PRIV;                // X2 with its rows staged (TMA slot)
 };
 
 template <int L>
@@ -37,13 +38,13 @@ void set_chain_attrs() {
   a((const void *)k_y1<L, true>, S::XPT);
   a((const void *)k_xq<L>, S::XPT);
   a((const void *)k_xg<L>, S::XPT);
-  a((const void *)k_x2<L, X2_GRAD, 0>, S::XH);
-  a((const void *)k_x2<L, X2_GRAD, 1>, S::XH);
-  a((const void *)k_x2<L, X2_GRAD, 2>, S::XH);
-  a((const void *)k_x2<L, X2_OBJ, 0>, S::XH);
-  a((const void *)k_x2<L, X2_OBJ, 1>, S::XH);
-  a((const void *)k_x2<L, X2_OBJ, 2>, S::XH);
-  a((const void *)k_x2<L, X2_FWD>, S::XH);
+  a((const void *)k_x2<L, X2_GRAD, 0>, S::XHS);
+  a((const void *)k_x2<L, X2_GRAD, 1>, S::XHS);
+  a((const void *)k_x2<L, X2_GRAD, 2>, S::XHS);
+  a((const void *)k_x2<L, X2_OBJ, 0>, S::XHS);
+  a((const void *)k_x2<L, X2_OBJ, 1>, S::XHS);
+  a((const void *)k_x2<L, X2_OBJ, 2>, S::XHS);
+  a((const void *)k_x2<L, X2_FWD>, S::XHS);
   a((const void *)k_x2<L, X2_ADJ>, S::XH);
   a((const void *)k_y2<L, false>, S::XPT);
   a((const void *)k_y2<L, true>, S::XPT);
@@ -351,25 +352,27 @@ struct Run {
         const dim3 g2(nbx2, HOLO_X2_LOOP ? 1 : nb);
         const size_t fo = (size_t)k0 * nz + j;  // first frame of the batch in [k][j] order
         pbeg(p);
+        const int x2s = (HOLO_X2_LOOP && p->w1map_ok) ? 1 : 0;  // rows staged by tensor copies
+        const size_t smx2 = x2s ? SM::XHS : SM::XH;
         if (mode == 1) {
-          k_x2<L, X2_FWD><<<g2, NT, SM::XH, p->stream>>>(p->W1, NL, nullptr, 0, wout + fo * NN, nz * NN, pf,
-                                                         nz * nbx2, tb, qh, N, p->tau, nb);
+          k_x2<L, X2_FWD><<<g2, NT, smx2, p->stream>>>(p->W1, NL, nullptr, 0, wout + fo * NN, nz * NN, pf,
+                                                       nz * nbx2, tb, qh, N, p->tau, nb, p->w1map, x2s);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
           continue;
         }
         if (mode == 3) {
-          (tm_ == 0 ? k_x2<L, X2_OBJ, 0> : tm_ == 1 ? k_x2<L, X2_OBJ, 1> : k_x2<L, X2_OBJ, 2>)<<<g2, NT, SM::XH, p->stream>>>(
-              p->W1, NL, sqrt_d + fo * NN, nz * NN, nullptr, 0, pf, nz * nbx2, tb, qh, N, p->tau, nb);
+          (tm_ == 0 ? k_x2<L, X2_OBJ, 0> : tm_ == 1 ? k_x2<L, X2_OBJ, 1> : k_x2<L, X2_OBJ, 2>)<<<g2, NT, smx2, p->stream>>>(
+              p->W1, NL, sqrt_d + fo * NN, nz * NN, nullptr, 0, pf, nz * nbx2, tb, qh, N, p->tau, nb, p->w1map, x2s);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8 / 2), nb * N * fl * 2);
           continue;
         }
         if (mode == 0) {
-          (tm_ == 0 ? k_x2<L, X2_GRAD, 0> : tm_ == 1 ? k_x2<L, X2_GRAD, 1> : k_x2<L, X2_GRAD, 2>)<<<g2, NT, SM::XH, p->stream>>>(
-              p->W1, NL, sqrt_d + fo * NN, nz * NN, p->V1, NL, pf, nz * nbx2, tb, qh, N, p->tau, nb);
+          (tm_ == 0 ? k_x2<L, X2_GRAD, 0> : tm_ == 1 ? k_x2<L, X2_GRAD, 1> : k_x2<L, X2_GRAD, 2>)<<<g2, NT, smx2, p->stream>>>(
+              p->W1, NL, sqrt_d + fo * NN, nz * NN, p->V1, NL, pf, nz * nbx2, tb, qh, N, p->tau, nb, p->w1map, x2s);
           pend(p, HOLO_PASS_X2, nb * (2 * rN * A + NN8 / 2), nb * N * fl * 4);
         } else {
           k_x2<L, X2_ADJ><<<g2, NT, SM::XH, p->stream>>>(yin + fo * NN, nz * NN, nullptr, 0, p->V1, NL, pf,
-                                                         nz * nbx2, tb, qh, N, p->tau, nb);
+                                                         nz * nbx2, tb, qh, N, p->tau, nb, p->w1map, 0);
           pend(p, HOLO_PASS_X2, nb * (rN * A + NN8), nb * N * fl * 2);
         }
         // ---- Y2 (batched): v = D_y^* V1[b]; G_j += conj(Aw[b]) v  (PS: Ut[b][j] = Hq_y^* FFT_y(conj(Aw) v));
