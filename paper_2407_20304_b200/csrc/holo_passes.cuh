@@ -93,26 +93,84 @@ __device__ __forceinline__ int stage_idx(int g, int y) { return 2 * L * (g >> 1)
 // rows of psi_k (row-major):  X = FFT(psi row) (kept thread-private); per j: T1_j row = M_{1/mt_j} S_{sx} psi row
 // (one non-inlined call per plane: only pointers and the pipe state cross it, so the
 // magnification keeps the whole register budget)
+// Row staging in X1 (HOLO_STAGE_X1, default 1; 2 <= G <= 8, launches without the fused CG update): a
+// launch covers the nb angles of a batch, each CTA looping over them for its G rows.  The rows of
+// angle b + 1 (row-major psi: G contiguous rows) are bulk-copied into the thread-private slot once
+// the last plane's second source read of angle b is behind a barrier (mag_fwd's src_freed hook), so
+// the CTA start (launch, table pipeline start, DRAM latency of the row loads) is paid once per batch
+// instead of once per angle.  Row g sits at g (L + 16/G) float2: the skew keeps a warp's (t, g) lanes
+// on distinct banks.
+#ifndef HOLO_STAGE_X1
+#define HOLO_STAGE_X1 1
+#endif
 template <int L>
+struct X1Stage {
+  static constexpr int SK = CtaK<L>::G <= 16 ? 16 / CtaK<L>::G : 1;  // float2
+  static constexpr int RS = L + SK;                                  // staged row stride
+  static constexpr bool OK = HOLO_STAGE && HOLO_STAGE_X1 && CtaK<L>::G >= 2 && CtaK<L>::G <= 8;
+  // control block at the end of the launch's dynamic shared memory (Smem::XPT1), so that the plane
+  // bodies find it from the shared-memory base instead of carrying it in registers
+  struct Ctl {
+    uint64_t bar;
+    const float2 *next;  // first of the CTA's rows of the next angle (nullptr: none)
+  };
+  static constexpr size_t CTL_OFF = CtaK<L>::XBYTES + CtaK<L>::PRIV + 128 + TabPipe<L>::BYTES;
+  __device__ __forceinline__ static Ctl *ctl(float2 *sm) {
+    return reinterpret_cast<Ctl *>(reinterpret_cast<char *>(sm) + CTL_OFF);
+  }
+  // thread 0, behind a CTA barrier that follows every thread's last access to the slot
+  __device__ __forceinline__ static void issue(float2 *sm, const float2 *rows) {
+    float2 *xs = priv_base<L>(sm);
+    uint64_t *bar = &ctl(sm)->bar;
+    fence_proxy_async();
+    mbar_expect_tx(bar, 8u * CtaK<L>::G * L);
+#pragma unroll 1
+    for (int g = 0; g < CtaK<L>::G; g++) bulk_g2s(xs + g * RS, rows + (size_t)g * L, 8u * L, bar);
+  }
+};
+
+template <int L, bool STG>
 __device__ __noinline__ TabPipe<L> x1_plane(float2 *__restrict__ T1j, const float4 *__restrict__ tw, const TabSeq &seq,
                                       TabPipe<L> pipe, float2 *sm, bool mag, bool sync0) {
   using C = CtaK<L>;
+  constexpr int T = L / 16;
   Xch x = C::xch(sm);
   const Priv<NT> X{priv_base<L>(sm)};
   const int t = C::t(), y = blockIdx.x * C::G + C::g();
+  // the spectrum of the row (thread-private smem), reused by every plane
+  auto src = [&](int r) -> float2 {
+    if constexpr (STG) {
+      const float2 z = priv_base<L>(sm)[C::g() * X1Stage<L>::RS + t + r * T];
+      if (r == 15) fence_proxy_async();  // this thread's slot accesses precede a later async write
+      return z;
+    } else {
+      return X[r];
+    }
+  };
+  auto freed = [&]() {
+    if constexpr (STG) {
+      if (threadIdx.x == 0) {
+        const float2 *nx = X1Stage<L>::ctl(sm)->next;  // set by the kernel for the angle's last plane
+        if (nx) {
+          X1Stage<L>::ctl(sm)->next = nullptr;
+          X1Stage<L>::issue(sm, nx);
+        }
+      }
+    }
+  };
   float2 v[16];
   if (mag) {
-    // X (thread-private smem) is reused by every plane: the first half's term stays in registers
+    // the first half's term stays in registers
     float2 e[16];
     mag_fwd<L>(
-        v, [&](int r) { return X[r]; }, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe, seq,
-        sync0, x, t, tw);
+        v, src, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe, seq, sync0, x, t, tw, freed);
   } else {
     const float2 *cr = pipe.take(seq, sync0);
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = cmul(X[r], cr[t + r * (L / 16)]);
+    for (int r = 0; r < 16; r++) v[r] = cmul(src(r), cr[t + r * T]);
     pipe.done(seq);
     fft<L, true>(v, x, t, tw);
+    freed();
   }
   st_p2_row<L>(v, T1j, y, L, t);
   return pipe;
@@ -171,7 +229,66 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     for (int r = 0; r < 16; r++) X[r] = v[r];
   }
 #pragma unroll 1
-  for (int j = 0; j < nz; j++) pipe = x1_plane<L>(T1 + (size_t)j * L * L, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j > 0);
+  for (int j = 0; j < nz; j++) pipe = x1_plane<L, false>(T1 + (size_t)j * L * L, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, j > 0);
+}
+
+// the staged rows -> their x-spectrum, in place (thread-private positions of the slot)
+template <int L>
+__device__ __noinline__ void x1_spectrum(float2 *sm, const float4 *__restrict__ tw) {
+  using C = CtaK<L>;
+  constexpr int T = L / 16;
+  Xch x = C::xch(sm);
+  float2 *xs = priv_base<L>(sm) + C::g() * X1Stage<L>::RS + C::t();
+  float2 v[16];
+#pragma unroll
+  for (int r = 0; r < 16; r++) v[r] = xs[r * T];
+  fft<L, false>(v, x, C::t(), tw);
+#pragma unroll
+  for (int r = 0; r < 16; r++) xs[r * T] = v[r];
+}
+
+// The staged, batched X1: the nb angles of a batch in one launch (psi0: the first angle, angles L^2
+// apart; T1 [nb][nz][L][L]), one flat loop over the (angle, plane) pairs so that little state is live
+// across the plane calls (kernel-level spills cost L2 round trips: the L1 left beside 198 KB of shared
+// memory does not hold the CTA's stack).
+template <int L>
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
+    k_x1s(const float2 *__restrict__ psi0, float2 *__restrict__ T1, Tables tb, const __grid_constant__ TabSeq seq,
+          int nz, uint32_t magmask, int fourier, int nb) {
+  using C = CtaK<L>;
+  using XS = X1Stage<L>;
+  extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  typename XS::Ctl *ctl = XS::ctl(sm);
+  if (threadIdx.x == 0) {
+    mbar_init(&ctl->bar, 1);
+    ctl->next = nullptr;
+    fence_mbar_init();
+  }
+  // [exchange][row slot: PRIV + 128 B (skewed rows)][table slots][control block]  (Smem::XPT1)
+  TabPipe<L> pipe;
+  pipe.start(seq, priv_base<L>(sm) + (C::PRIV + 128) / sizeof(float2), bars);
+  __syncthreads();
+  if (threadIdx.x == 0) XS::issue(sm, psi0 + (size_t)blockIdx.x * C::G * L);
+  const int nm = nb * nz;
+#pragma unroll 1
+  for (int m = 0, j = 0, b = 0; m < nm; m++) {
+    if (j == 0) {  // a new angle: its rows have been staged
+      if (threadIdx.x == 0 && b + 1 < nb)  // the copy at the end of this angle reads L2
+        prefetch_l2(psi0 + ((size_t)(b + 1) * L + (size_t)blockIdx.x * C::G) * L, 8u * C::G * L);
+      mbar_wait(&ctl->bar, b & 1);
+      if (!fourier) x1_spectrum<L>(sm, tb.tw);  // HOLO_FOURIER: the row of DFT2(psi) IS the x-spectrum
+    }
+    // the last plane's src_freed hook (thread 0) copies the next angle's rows
+    if (j + 1 == nz && threadIdx.x == 0)
+      ctl->next = b + 1 < nb ? psi0 + ((size_t)(b + 1) * L + (size_t)blockIdx.x * C::G) * L : nullptr;
+    pipe = x1_plane<L, XS::OK>(T1 + (size_t)m * L * L, tb.tw, seq, pipe, sm, (magmask >> j) & 1u, m > 0);
+    if (++j == nz) {
+      j = 0;
+      b++;
+    }
+  }
 }
 
 // ----------------------------------------------------------------------------- Y1

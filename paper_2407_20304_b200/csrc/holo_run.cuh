@@ -22,6 +22,7 @@ struct Smem {
   static constexpr size_t XPT = X + CtaK<L>::PRIV + TabPipe<L>::BYTES;  // + one thread-private line
   static constexpr size_t XH = X + sizeof(float2) * L;                   // + X2's resident table
   static constexpr size_t XPT3 = XPT + 128;                              // X3: private slot 128-byte aligned
+  static constexpr size_t XPT1 = XPT + 128 + 16;                         // X1: row slot with skewed rows + control block
   static constexpr size_t XHS = XH + 128 + CtaK<L>::PRIV;                // X2 with its rows staged (TMA slot)
 };
 
@@ -30,6 +31,7 @@ void set_chain_attrs() {
   using S = Smem<L>;
   auto a = [](const void *f, size_t s) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s); };
   a((const void *)k_x1<L>, S::XPT);
+  a((const void *)k_x1s<L>, S::XPT1);
   a((const void *)k_dft2_rows<L, false>, S::X);
   a((const void *)k_dft2_rows<L, true>, S::X);
   a((const void *)k_dft2_cols<L, false>, S::X);
@@ -284,7 +286,24 @@ struct Run {
       const int nb = K - k0 < p->B ? K - k0 : p->B;  // ragged last batch
       // ---- X1 (per angle): T1[b][j] = (M S)_x psi_k rows;  PS: XQ, Qt[b][j] = IFFT_x(Hq_x Qhat)
       if (need_fwd_chain) {
-        for (int b = 0; b < nb; b++) {
+        // one launch for the batch (each CTA loops over the angles, the next angle's rows staged behind the
+        // last plane) when the chained table sequence fits and the CG update is not fused; else per angle
+        const int tabs_per_angle = 5 * nmag + (nz - nmag);
+        const bool x1b = X1Stage<L>::OK && cgf.mode < 0 && nb * tabs_per_angle <= MAXTAB;
+        if (x1b) {
+          TabSeq q{};
+          for (int b = 0; b < nb; b++)
+            for (int j = 0; j < nz; j++) {
+              if ((p->magmask >> j) & 1u)
+                add_fwd(q, k0 + b, j, 0);
+              else
+                q.p[q.n++] = crp(k0 + b, j, 0);
+            }
+          pbeg(p);
+          k_x1s<L><<<L / G, NT, SM::XPT1, p->stream>>>(psi_src + (size_t)k0 * LL, p->T1, tb, q, nz, p->magmask, fo_, nb);
+          pend(p, HOLO_PASS_X1, nb * (1 + nz) * A, nb * L * fl * ((fo_ ? 0 : 1) + 4 * nmag + (nz - nmag)));
+        }
+        for (int b = 0; b < (x1b ? 0 : nb); b++) {
           const int k = k0 + b;
           TabSeq q{};
           for (int j = 0; j < nz; j++) {

@@ -5,7 +5,7 @@ TAG=${TAG:-v}
 for lib in paper_2407_20304_b200/libholo.so ${VARIANTS:-build_variants/*.so}; do
   echo "== $lib"
   HOLO_LIB=$lib timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_cg.py -x -q -m gpu -k "not full_size" 2>&1 | tail -1
-  HOLO_LIB=$lib timeout 600 python bench.py --angles $ANG --steps 2 --warmup 2 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
+  HOLO_LIB=$lib timeout 150 python bench.py --angles $ANG --steps 2 --warmup 2 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read().strip().splitlines()[-1])
 print('value %.1f frame-it/s  ms/step %.1f' % (d['value'], d['ms_per_step']))
