@@ -1056,6 +1056,206 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   }
 }
 
+// The batched X3 (HOLO_X3_BATCH, default 1; needs the T3 tensor map): one launch for the nb angles of a
+// batch, each CTA looping over the (angle, plane) pairs for its G rows.  The tensor copy of pair m + 1
+// is issued from pair m's src_freed hook also across an angle boundary, and the angle's tail (plane
+// sum, scale, g row, the two dots) runs inside the last plane's body on the values in registers, so the
+// slot is free for that copy.  Per-launch / per-angle state sits in a control block in shared memory
+// (the plane body finds it from the shared-memory base; kernel-level spills cost L2 round trips here).
+#ifndef HOLO_X3_BATCH
+#define HOLO_X3_BATCH 1
+#endif
+#ifndef HOLO_X3_WJ
+#define HOLO_X3_WJ 0  // 1: plane terms stored in place of the consumed T3 rows and summed in the tail (measured slower: X3 222 vs 191 us/frame); 0: L2 reductions into g
+#endif
+template <int L>
+struct X3Ctl {
+  uint64_t bar;
+  const CUtensorMap *map;
+  float2 *t3;         // the T3 workspace (plane 0 of the map)
+  const float2 *eta;  // this angle's eta (nullptr: none), g and partials
+  float2 *g;
+  double *partial;
+  float scale;
+  int next;  // plane index (in the map) of the next copy, -1: none
+  static constexpr size_t OFF = CtaK<L>::XBYTES + CtaK<L>::PRIV + 128 + TabPipe<L>::BYTES;  // after Smem::XPT3
+  __device__ __forceinline__ static X3Ctl *at(float2 *sm) {
+    return reinterpret_cast<X3Ctl *>(reinterpret_cast<char *>(sm) + OFF);
+  }
+};
+template <int L>
+__device__ __forceinline__ float2 *x3_slot(float2 *sm) {
+  float2 *pv = priv_base<L>(sm);
+  return pv + ((128u - (smem_u32(pv) & 127u)) & 127u) / sizeof(float2);
+}
+enum { X3F_MAG = 1, X3F_SYNC0 = 2, X3F_FIRST = 4, X3F_LAST = 8, X3F_FOURIER = 16, X3F_PHASE = 32 };
+
+template <int L>
+__device__ __noinline__ TabPipe<L> x3s_plane(const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> pipe,
+                                       float2 *sm, int flags) {  // flags: X3F_* | j << 8 | map plane << 16
+  using C = CtaK<L>;
+  constexpr int T = L / 16;
+  __shared__ double red[32];
+  Xch x = C::xch(sm);
+  const int t = C::t();
+  float2 v[16];
+  {
+    // element (y0 + g, x = t + r T) of the staged rows at 2 (G (x >> 1) + g) + (x & 1); T is even
+    const float2 *zb = x3_slot<L>(sm) + 2 * (C::G * (t >> 1) + C::g()) + (t & 1);
+    auto S = [&](int r) { return zb[r * (C::G * T)]; };
+    // the next pair's tensor copies, one per thread (no loop state beside the transforms' registers)
+    auto freed = [&]() {
+      constexpr int BOXC = L / 2 < 256 ? L / 2 : 256, NC = (L / 2) / BOXC;
+      const int i = threadIdx.x;
+      if (i < NC) {
+        X3Ctl<L> *c = X3Ctl<L>::at(sm);
+        const int nx = c->next;
+        if (nx >= 0) {
+          if (i == 0) mbar_expect_tx(&c->bar, 8u * C::G * L);
+          tma_load_4d(x3_slot<L>(sm) + 2 * C::G * BOXC * i, c->map, 0, (int)(blockIdx.x * C::G), BOXC * i, nx, &c->bar);
+        }
+      }
+    };
+    mbar_wait(&X3Ctl<L>::at(sm)->bar, (flags & X3F_PHASE) ? 1u : 0u);
+    if (flags & X3F_MAG) {
+      float2 e[16];
+      mag_adj<L>(
+          v, S, [&](int r, float2 val) { e[r] = val; }, [&](int r) { return e[r]; }, pipe, seq, (flags & X3F_SYNC0) != 0, x,
+          t, tw, freed);
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = S(r);
+      fft<L, false>(v, x, t, tw);
+      freed();
+      const float2 *cr = pipe.take(seq);
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cmulc(v[r], cr[t + r * T]);
+      pipe.done(seq);
+    }
+  }
+  const X3Ctl<L> *c = X3Ctl<L>::at(sm);
+  const size_t row = (size_t)(blockIdx.x * C::G + C::g()) * L + t;
+  float2 *grow = c->g + row;  // also the Fourier-domain accumulator of sum_j W_j (one owner thread per element)
+#if HOLO_X3_WJ
+  // W_j overwrites this CTA's (consumed) rows of its T3 plane with plain stores; the angle's tail sums
+  // the planes (one round trip of independent L2 reads) instead of nz - 1 rounds of L2 reductions
+  const int pl = flags >> 16, nprev = (flags >> 8) & 0xff;
+  if (!(flags & X3F_LAST)) {
+    st_p2_row<L>(v, c->t3 + (size_t)pl * L * L, blockIdx.x * C::G + C::g(), L, t);
+    return pipe;
+  }
+  {
+    const float2 *w0 = c->t3 + (size_t)(pl - nprev) * L * L;
+    const int y = blockIdx.x * C::G + C::g();
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const size_t i = p2(y, t + r * T, L);
+      float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int jj = 0; jj < HOLO_MAX_NZ - 1; jj++)
+        if (jj < nprev) acc = cadd(acc, __ldcg(w0 + (size_t)jj * L * L + i));
+      v[r] = cadd(acc, v[r]);
+    }
+    flags |= X3F_FIRST;  // the sum is complete: nothing to read back from the g row
+  }
+#else
+  if (!(flags & X3F_LAST)) {
+    if (flags & X3F_FIRST) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) grow[r * T] = v[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; r++) red_add2(grow + r * T, v[r]);
+    }
+    return pipe;
+  }
+#endif
+  // the angle's tail: the earlier planes' sum (L2) and eta are fetched together
+  const float2 *erow = c->eta ? c->eta + row : nullptr;
+  const float scale = c->scale;
+  double gg = 0.0, ge = 0.0;
+  if (flags & X3F_FOURIER) {
+#pragma unroll
+    for (int r = 0; r < 16; r++) {  // (the loads of several r are in flight together)
+      const float2 sv = (flags & X3F_FIRST) ? make_float2(0.f, 0.f) : __ldcg(grow + r * T);
+      const float2 ev = erow ? ldg2(erow + r * T) : make_float2(0.f, 0.f);
+      const float2 a = cscale(cadd(sv, v[r]), scale);
+      grow[r * T] = a;
+      gg += (double)(a.x * a.x + a.y * a.y);
+      ge += (double)(a.x * ev.x + a.y * ev.y);
+    }
+  } else {
+    if (!(flags & X3F_FIRST)) {
+#pragma unroll
+      for (int r = 0; r < 16; r++) v[r] = cadd(__ldcg(grow + r * T), v[r]);
+    }
+    fft<L, true>(v, x, t, tw);
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const float2 a = cscale(v[r], scale);
+      grow[r * T] = a;
+      gg += (double)(a.x * a.x + a.y * a.y);
+      if (erow) {
+        const float2 e = ldg2(erow + r * T);
+        ge += (double)(a.x * e.x + a.y * e.y);
+      }
+    }
+  }
+  const double s0 = block_sum(gg, red);
+  const double s1 = block_sum(ge, red);
+  if (threadIdx.x == 0) {
+    const double ps = (flags & X3F_FOURIER) ? 1.0 / ((double)L * L) : 1.0;  // Parseval: object-domain dots
+    c->partial[2 * blockIdx.x] = s0 * ps;
+    c->partial[2 * blockIdx.x + 1] = s1 * ps;
+  }
+  return pipe;
+}
+
+// T3 [nb][nz][L][L] (map planes pl0 ...), eta / g: the batch's first angle (angles L^2 apart),
+// partial: 2 gridDim.x doubles per angle
+template <int L>
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
+    k_x3s(float2 *__restrict__ T3, const float2 *__restrict__ eta, float2 *__restrict__ g, double *__restrict__ partial, Tables tb,
+          const __grid_constant__ TabSeq seq, int nz, uint32_t magmask, float scale, int fourier,
+          const __grid_constant__ CUtensorMap t3map, int pl0, int nb) {
+  using C = CtaK<L>;
+  extern __shared__ float4 sm4[];
+  __shared__ uint64_t bars[2];
+  float2 *sm = reinterpret_cast<float2 *>(sm4);
+  X3Ctl<L> *ctl = X3Ctl<L>::at(sm);
+  if (threadIdx.x == 0) {
+    mbar_init(&ctl->bar, 1);
+    ctl->map = &t3map;
+    ctl->t3 = T3;
+    ctl->scale = scale;
+    ctl->next = -1;
+    fence_mbar_init();
+  }
+  // [exchange][<= 112 B pad][private slot, 128-byte aligned: TMA destination][table slots][control block]
+  TabPipe<L> pipe;
+  pipe.start(seq, x3_slot<L>(sm) + C::PRIV / sizeof(float2), bars);
+  __syncthreads();
+  RowStage{&t3map, &ctl->bar, -1, (int)(blockIdx.x * C::G), 0}.template issue<L>(x3_slot<L>(sm), pl0);
+#pragma unroll 1
+  for (int m = 0; m < nb * nz; m++) {
+    const int b = m / nz, j = m - b * nz;
+    if (threadIdx.x == 0) {
+      if (j == 0) {  // a new angle (every thread is past the previous angle's tail barriers)
+        const size_t ao = (size_t)b * L * L;
+        ctl->eta = eta ? eta + ao : nullptr;
+        ctl->g = g + ao;
+        ctl->partial = partial + (size_t)b * 2 * gridDim.x;
+        if (eta) prefetch_l2(eta + ao + (size_t)blockIdx.x * C::G * L, 8u * C::G * L);  // read in the angle's tail
+      }
+      ctl->next = m + 1 < nb * nz ? pl0 + m + 1 : -1;
+    }
+    const int flags = (((magmask >> j) & 1u) ? X3F_MAG : 0) | (m > 0 ? X3F_SYNC0 : 0) | (j == 0 ? X3F_FIRST : 0) |
+                      (j + 1 == nz ? X3F_LAST : 0) | (fourier ? X3F_FOURIER : 0) | ((m & 1) ? X3F_PHASE : 0) | (j << 8) |
+                      ((pl0 + m) << 16);
+    pipe = x3s_plane<L>(tb.tw, seq, pipe, sm, flags);
+  }
+}
+
 // ----------------------------------------------------------------------------- XQ, XG (PS)
 // Per-frame probe shifts (O19): with Qhat = DFT2 q (P2 [fy][fx]) and Hq(k,j) = h_omega_j r_{s^p_kj} / L
 // per axis, q_kj = IDFT_y(Hq_y IDFT_x(Hq_x Qhat)).

@@ -22,6 +22,7 @@ struct Smem {
   static constexpr size_t XPT = X + CtaK<L>::PRIV + TabPipe<L>::BYTES;  // + one thread-private line
   static constexpr size_t XH = X + sizeof(float2) * L;                   // + X2's resident table
   static constexpr size_t XPT3 = XPT + 128;                              // X3: private slot 128-byte aligned
+  static constexpr size_t XPT3S = XPT3 + 64;                             // batched X3: + control block
   static constexpr size_t XPT1 = XPT + 128 + 16;                         // X1: row slot with skewed rows + control block
   static constexpr size_t XHS = XH + 128 + CtaK<L>::PRIV;                // X2 with its rows staged (TMA slot)
 };
@@ -51,6 +52,7 @@ void set_chain_attrs() {
   a((const void *)k_y2<L, false>, S::XPT);
   a((const void *)k_y2<L, true>, S::XPT);
   a((const void *)k_x3<L>, S::XPT3);
+  a((const void *)k_x3s<L>, S::XPT3S);
   a((const void *)k_rows_filter<L, false, true, false>, S::X);
   a((const void *)k_rows_filter<L, true, false, false>, S::X);
   a((const void *)k_rows_filter<L, true, false, true>, S::X);
@@ -454,16 +456,34 @@ struct Run {
                                                     p->t3map, b * nz, p->t3map_ok ? 1 : 0);
         pend(p, HOLO_PASS_X3, (nz + 1 + (eta ? 1 : 0)) * A, L * fl * (4 * nmag + (nz - nmag) + (fo_ ? 0 : 1)));
       };
+      // one launch for the batch (k_x3s) when the T3 tensor map exists and the chained tables fit
+      auto x3all = [&]() {
+        if (HOLO_STAGE && HOLO_X3_BATCH && G >= 2 && p->t3map_ok && nb * (5 * nmag + (nz - nmag)) <= MAXTAB) {
+          TabSeq q3{};
+          for (int b = 0; b < nb; b++)
+            for (int j = 0; j < nz; j++) {
+              if ((p->magmask >> j) & 1u)
+                add_adj(q3, k0 + b, j, 0);
+              else
+                q3.p[q3.n++] = crp(k0 + b, j, 0);
+            }
+          pbeg(p);
+          k_x3s<L><<<L / G, NT, SM::XPT3S, p->stream>>>(p->T3, eta ? eta + (size_t)k0 * LL : nullptr, gpsi + (size_t)k0 * LL,
+                                                        p->partX3 + (size_t)k0 * 2 * p->nbx3, tb, q3, nz, p->magmask,
+                                                        fo_ ? gscale * (float)L * (float)L : gscale, fo_, p->t3map, 0, nb);
+          pend(p, HOLO_PASS_X3, nb * (nz + 1 + (eta ? 1 : 0)) * A, nb * L * fl * (4 * nmag + (nz - nmag) + (fo_ ? 0 : 1)));
+        } else {
+          for (int b = 0; b < nb; b++) x3(b);
+        }
+      };
       const bool want_x3 = gpsi && (mode == 0 || mode == 2);
       if (!last_batch) {
-        if (want_x3)
-          for (int b = 0; b < nb; b++) x3(b);
+        if (want_x3) x3all();
         if (ps && gq_pass) xg();
       } else {
         if (ps && gq_pass) xg();
         finish_q(p, q, gq_out, gscale, want_q, acc_q, mode, sqrt_dref);
-        if (want_x3)
-          for (int b = 0; b < nb; b++) x3(b);
+        if (want_x3) x3all();
       }
     }
     if (K == 0) finish_q(p, q, gq_out, gscale, want_q, acc_q, mode, sqrt_dref);
