@@ -68,7 +68,7 @@ __device__ __forceinline__ void st_p2_col(const float2 (&v)[16], float2 *__restr
 #define HOLO_STAGE 1
 #endif
 #ifndef HOLO_STAGE_Q
-#define HOLO_STAGE_Q 1  // Y1: the q_j block through the slot too (bulk copy behind the magnification)
+#define HOLO_STAGE_Q 1  // Y1: the q_j block through the slot too (1: behind the magnification; 2: also in the shift-only plane)
 #endif
 struct ColStage {
   uint64_t *bar;       // the slot's mbarrier
@@ -355,6 +355,17 @@ __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const
 #pragma unroll
     for (int r = 0; r < 16; r++) v[r] = cmul(v[r], cr[t + r * T]);
     pipe.done(seq);
+    if constexpr (STG) {
+      if (st.qblk) {  // shift-only plane: the q_j block lands behind the one inverse transform
+        fence_proxy_async();
+        __syncthreads();  // every thread is past its reads of the staged column
+        if (threadIdx.x == 0) {
+          fence_proxy_async();
+          mbar_expect_tx(st.bar, st.bytes);
+          bulk_g2s(Sb, st.qblk, st.bytes, st.bar);
+        }
+      }
+    }
     fft<L, true>(v, x, t, tw);
   }
   if (aout) st_p2_col<L>(v, aout, col, L, t);
@@ -373,7 +384,7 @@ __device__ __noinline__ TabPipe<L> y1_frame(const float2 *__restrict__ in, const
       for (int r = 0; r < 16; r++) v[r] = cmul(v[r], X[r]);
     }
   } else if (w1) {
-    if (STG && mag && st.qblk) {
+    if (STG && st.qblk) {
       mbar_wait(st.bar, 1);
 #pragma unroll
       for (int r = 0; r < 16; r++) v[r] = cmul(v[r], slot(r));
@@ -432,7 +443,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
   }
   constexpr int PF_COLS = C::G < 2 ? 2 : C::G;  // whole P2 column pairs (16-byte aligned blocks)
-  const bool qstg = STG && HOLO_STAGE_Q && mag && W1 && qj;  // q_j staged behind the magnification
+  // q_j staged behind the magnification (HOLO_STAGE_Q >= 1) / the shift-only plane's transform (2)
+  const bool qstg = STG && HOLO_STAGE_Q && (mag || HOLO_STAGE_Q >= 2) && W1 && qj;
 #pragma unroll 1
   for (int b = 0; b < nb; b++) {
     const float2 *in = T1j + (size_t)b * fstride;
@@ -1065,6 +1077,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 #ifndef HOLO_X3_BATCH
 #define HOLO_X3_BATCH 1
 #endif
+#ifndef HOLO_X3_PF
+#define HOLO_X3_PF 1  // tensor prefetch (L2) of the next (angle, plane) pair's rows at the start of each pair
+#endif
 #ifndef HOLO_X3_WJ
 #define HOLO_X3_WJ 0  // 1: plane terms stored in place of the consumed T3 rows and summed in the tail (measured slower: X3 222 vs 191 us/frame); 0: L2 reductions into g
 #endif
@@ -1077,7 +1092,6 @@ struct X3Ctl {
   float2 *g;
   double *partial;
   float scale;
-  int next;  // plane index (in the map) of the next copy, -1: none
   static constexpr size_t OFF = CtaK<L>::XBYTES + CtaK<L>::PRIV + 128 + TabPipe<L>::BYTES;  // after Smem::XPT3
   __device__ __forceinline__ static X3Ctl *at(float2 *sm) {
     return reinterpret_cast<X3Ctl *>(reinterpret_cast<char *>(sm) + OFF);
@@ -1088,7 +1102,7 @@ __device__ __forceinline__ float2 *x3_slot(float2 *sm) {
   float2 *pv = priv_base<L>(sm);
   return pv + ((128u - (smem_u32(pv) & 127u)) & 127u) / sizeof(float2);
 }
-enum { X3F_MAG = 1, X3F_SYNC0 = 2, X3F_FIRST = 4, X3F_LAST = 8, X3F_FOURIER = 16, X3F_PHASE = 32 };
+enum { X3F_MAG = 1, X3F_SYNC0 = 2, X3F_FIRST = 4, X3F_LAST = 8, X3F_FOURIER = 16, X3F_PHASE = 32, X3F_NEXT = 64 };
 
 template <int L>
 __device__ __noinline__ TabPipe<L> x3s_plane(const float4 *__restrict__ tw, const TabSeq &seq, TabPipe<L> pipe,
@@ -1104,18 +1118,22 @@ __device__ __noinline__ TabPipe<L> x3s_plane(const float4 *__restrict__ tw, cons
     const float2 *zb = x3_slot<L>(sm) + 2 * (C::G * (t >> 1) + C::g()) + (t & 1);
     auto S = [&](int r) { return zb[r * (C::G * T)]; };
     // the next pair's tensor copies, one per thread (no loop state beside the transforms' registers)
+    constexpr int BOXC = L / 2 < 256 ? L / 2 : 256, NC = (L / 2) / BOXC;
     auto freed = [&]() {
-      constexpr int BOXC = L / 2 < 256 ? L / 2 : 256, NC = (L / 2) / BOXC;
       const int i = threadIdx.x;
-      if (i < NC) {
+      if (i < NC && (flags & X3F_NEXT)) {
         X3Ctl<L> *c = X3Ctl<L>::at(sm);
-        const int nx = c->next;
-        if (nx >= 0) {
-          if (i == 0) mbar_expect_tx(&c->bar, 8u * C::G * L);
-          tma_load_4d(x3_slot<L>(sm) + 2 * C::G * BOXC * i, c->map, 0, (int)(blockIdx.x * C::G), BOXC * i, nx, &c->bar);
-        }
+        if (i == 0) mbar_expect_tx(&c->bar, 8u * C::G * L);
+        tma_load_4d(x3_slot<L>(sm) + 2 * C::G * BOXC * i, c->map, 0, (int)(blockIdx.x * C::G), BOXC * i,
+                    (flags >> 16) + 1, &c->bar);
       }
     };
+#if HOLO_X3_PF
+    // the next pair's rows into L2 now (a tensor prefetch: 2048 strided 32-byte pieces from DRAM), so the
+    // copy issued from the src_freed hook, one transform before it is needed, reads L2
+    if ((int)threadIdx.x < NC && (flags & X3F_NEXT))
+      tma_prefetch_4d(X3Ctl<L>::at(sm)->map, 0, (int)(blockIdx.x * C::G), BOXC * threadIdx.x, (flags >> 16) + 1);
+#endif
     mbar_wait(&X3Ctl<L>::at(sm)->bar, (flags & X3F_PHASE) ? 1u : 0u);
     if (flags & X3F_MAG) {
       float2 e[16];
@@ -1175,14 +1193,20 @@ __device__ __noinline__ TabPipe<L> x3s_plane(const float4 *__restrict__ tw, cons
   const float scale = c->scale;
   double gg = 0.0, ge = 0.0;
   if (flags & X3F_FOURIER) {
+    // all reads first: the g-row stores below alias the g-row reads, so a single loop would wait for
+    // one L2 round trip per element (measured: 9 % of the pass)
 #pragma unroll
-    for (int r = 0; r < 16; r++) {  // (the loads of several r are in flight together)
-      const float2 sv = (flags & X3F_FIRST) ? make_float2(0.f, 0.f) : __ldcg(grow + r * T);
-      const float2 ev = erow ? ldg2(erow + r * T) : make_float2(0.f, 0.f);
-      const float2 a = cscale(cadd(sv, v[r]), scale);
+    for (int r = 0; r < 16; r++)
+      if (!(flags & X3F_FIRST)) v[r] = cadd(__ldcg(grow + r * T), v[r]);
+    float2 ev[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) ev[r] = erow ? ldg2(erow + r * T) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const float2 a = cscale(v[r], scale);
       grow[r * T] = a;
       gg += (double)(a.x * a.x + a.y * a.y);
-      ge += (double)(a.x * ev.x + a.y * ev.y);
+      ge += (double)(a.x * ev[r].x + a.y * ev[r].y);
     }
   } else {
     if (!(flags & X3F_FIRST)) {
@@ -1190,15 +1214,15 @@ __device__ __noinline__ TabPipe<L> x3s_plane(const float4 *__restrict__ tw, cons
       for (int r = 0; r < 16; r++) v[r] = cadd(__ldcg(grow + r * T), v[r]);
     }
     fft<L, true>(v, x, t, tw);
+    float2 ev[16];
+#pragma unroll
+    for (int r = 0; r < 16; r++) ev[r] = erow ? ldg2(erow + r * T) : make_float2(0.f, 0.f);
 #pragma unroll
     for (int r = 0; r < 16; r++) {
       const float2 a = cscale(v[r], scale);
       grow[r * T] = a;
       gg += (double)(a.x * a.x + a.y * a.y);
-      if (erow) {
-        const float2 e = ldg2(erow + r * T);
-        ge += (double)(a.x * e.x + a.y * e.y);
-      }
+      ge += (double)(a.x * ev[r].x + a.y * ev[r].y);
     }
   }
   const double s0 = block_sum(gg, red);
@@ -1228,7 +1252,6 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     ctl->map = &t3map;
     ctl->t3 = T3;
     ctl->scale = scale;
-    ctl->next = -1;
     fence_mbar_init();
   }
   // [exchange][<= 112 B pad][private slot, 128-byte aligned: TMA destination][table slots][control block]
@@ -1247,10 +1270,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         ctl->partial = partial + (size_t)b * 2 * gridDim.x;
         if (eta) prefetch_l2(eta + ao + (size_t)blockIdx.x * C::G * L, 8u * C::G * L);  // read in the angle's tail
       }
-      ctl->next = m + 1 < nb * nz ? pl0 + m + 1 : -1;
     }
     const int flags = (((magmask >> j) & 1u) ? X3F_MAG : 0) | (m > 0 ? X3F_SYNC0 : 0) | (j == 0 ? X3F_FIRST : 0) |
-                      (j + 1 == nz ? X3F_LAST : 0) | (fourier ? X3F_FOURIER : 0) | ((m & 1) ? X3F_PHASE : 0) | (j << 8) |
+                      (j + 1 == nz ? X3F_LAST : 0) | (fourier ? X3F_FOURIER : 0) | ((m & 1) ? X3F_PHASE : 0) |
+                      (m + 1 < nb * nz ? X3F_NEXT : 0) | (j << 8) |
                       ((pl0 + m) << 16);
     pipe = x3s_plane<L>(tb.tw, seq, pipe, sm, flags);
   }

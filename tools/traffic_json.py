@@ -11,7 +11,7 @@ import sys
 from collections import defaultdict
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-PASS = {"k_x1": "X1", "k_y1": "Y1", "k_x2": "X2", "k_y2": "Y2", "k_x3": "X3", "k_ref": "ref"}
+PASS = {"k_x1": "X1", "k_x1s": "X1", "k_y1": "Y1", "k_x2": "X2", "k_y2": "Y2", "k_x3": "X3", "k_x3s": "X3", "k_ref": "ref"}
 
 
 def main(rep, out, workload="cfg3", batch=8):
