@@ -243,6 +243,32 @@ def test_angle_batch_ragged_parity(batch):
     assert abs(s[2] - ge) / abs(ge) < TOL_S
 
 
+@pytest.mark.parametrize("K,batch,fourier", [(17, 16, False), (17, 16, True), (7, 3, True), (5, 2, False)])
+def test_angle_batch_extremes_parity(K, batch, fourier):
+    """The largest angle batch the ABI accepts (16) with a one-angle tail (K = 17), and odd batches with
+    ragged tails (7 = 3 + 3 + 1, 5 = 2 + 2 + 1), at cfg1 (512^2 torus, 4 planes): the batched X1 / X3 launches stage the next
+    (angle, plane) pair's rows across angle boundaries, so every boundary position is exercised.  F,
+    grad_psi, grad_q, the fused scalars vs the numpy oracle, in the object and the Fourier-domain state."""
+    c = Case("cfg1", K, oracle_kind="np")
+    p = make_plan(c.cfg, c.K, batch=batch)
+    p.set_shifts(c.s)
+    F, gp, gq = c.oracle_grad()
+    eta = correlated_eta(gp, seed=K + batch)
+    f2 = (lambda a: np.fft.fft2(a, axes=(-2, -1))) if fourier else (lambda a: a)
+    if fourier:
+        p.set_fourier(True)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    gpsi = torch.empty(c.psi.shape, dtype=torch.complex64, device="cuda")
+    gqd = torch.empty(c.q.shape, dtype=torch.complex64, device="cuda")
+    p.grad(dev(f2(c.psi)), dev(c.q), dev(c.d, torch.float32), sc, dev(f2(eta.astype(np.complex128))), gpsi, gqd)
+    s = host(sc).real
+    assert abs(s[0] - F) / F < TOL_S
+    assert rel(host(gpsi), f2(gp)) < TOL_G and rel(host(gqd), gq) < TOL_G
+    assert abs(s[1] - np.vdot(gp, gp).real) / np.vdot(gp, gp).real < TOL_S
+    ge = np.vdot(eta.astype(np.complex128), gp).real
+    assert abs(s[2] - ge) / abs(ge) < TOL_S
+
+
 def test_accumulate_q_flag(cfg0):
     """HOLO_ACCUMULATE_Q adds the probe-gradient partial into grad_q_part (SURVEY 8b flag)."""
     import paper_2407_20304_b200 as hb
